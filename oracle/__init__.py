@@ -1,0 +1,235 @@
+"""CPU oracle for the parallel cross-validation loss (Gerber & Nychka, arXiv 1912.13132).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this package.
+The product path (``paper_1912_13132_b200``) never imports, links or calls it, and the
+two share no code: this is the plain definition of Eq.7 evaluated by
+Algorithm 1, written in ``oracle.c`` (fp64, ``-ffp-contract=off``) and driven
+from here with ctypes.  Every function cites the passage it follows; DESIGN.md lists the
+readings (R1..R18) taken where the paper is silent.
+
+Pins (tests/test_oracle_pins.py, all ``-m "not gpu"``): closed-form kriging for k = 1, 2,
+3; exp-covariance values; interpolation at observed sites with zero nugget; far-field
+zero prediction; N = 1 and delta-saturation exactness (Eq.7 == Eq.4); power-of-two
+metamorphic invariants (bit-exact); permutation invariance; partition invariants and
+hand-worked golden partitions (tests/golden/).  The per-config global losses at the
+BASELINE sizes c2..c5 have no printed value in the paper: "parity unpinned" beyond the
+agreement of the two independent implementations.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, EINVAL, ENUMERIC, ENOMEM = 0, -2, -3, -6
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc -O2 -ffp-contract=off; no FMA, IEEE doubles)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+               "-std=c11", "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            d, i32, i64, p = ctypes.c_double, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+            lib.oracle_edges.argtypes = [d, d, i32, p]
+            lib.oracle_partition_count.argtypes = [i64, p, p, p, d, d, d, d, i32, i32, d, p, p]
+            lib.oracle_partition_fill.argtypes = [i64, p, p, p, d, d, d, d, i32, i32, d, p, p, p, p]
+            for f in (lib.oracle_subset_cv, lib.oracle_subset_cv_ld):
+                f.argtypes = [i64, p, p, p, i64, p, p, p, d, d, d, p]
+            lib.oracle_neg2loglik.argtypes = [i64, p, p, p, d, d, d, p]
+            _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"oracle {what} failed with code {code}")
+        self.code = code
+
+
+def edges(a: float, b: float, K: int) -> np.ndarray:
+    """Tile edges e_0..e_K of [a, b) in K equal tiles (reading R4; P:242-246 divides D)."""
+    e = np.empty(K + 1, np.float64)
+    rc = _load().oracle_edges(a, b, K, _ptr(e))
+    if rc:
+        raise OracleError(rc, "edges")
+    return e
+
+
+class Partition:
+    """CSR membership lists of Alg.1 lines 2-3: train (core + shell)
+    and validation (core only, Eq.7) per subset s = iy*kx + ix."""
+
+    def __init__(self, train_off, train_idx, val_off, val_idx, kx, ky):
+        self.train_off, self.train_idx = train_off, train_idx
+        self.val_off, self.val_idx = val_off, val_idx
+        self.kx, self.ky = kx, ky
+
+    @property
+    def n_subsets(self) -> int:
+        return self.kx * self.ky
+
+    def k(self) -> np.ndarray:
+        return np.diff(self.train_off)
+
+    def m(self) -> np.ndarray:
+        return np.diff(self.val_off)
+
+    def train(self, s: int) -> np.ndarray:
+        return self.train_idx[self.train_off[s]:self.train_off[s + 1]]
+
+    def val(self, s: int) -> np.ndarray:
+        return self.val_idx[self.val_off[s]:self.val_off[s + 1]]
+
+
+def partition(x, y, role, domain, kx: int, ky: int, delta: float) -> Partition:
+    """Brute-force subset membership (Alg.1 lines 2-3; shell of width delta, P:154-159;
+    readings R1-R6).  Every point is tested against every tile interval on each axis."""
+    lib = _load()
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    role = np.ascontiguousarray(role, np.uint8)
+    n = x.shape[0]
+    N = kx * ky
+    tc = np.zeros(N, np.int64)
+    vc = np.zeros(N, np.int64)
+    xmin, xmax, ymin, ymax = (float(v) for v in domain)
+    rc = lib.oracle_partition_count(n, _ptr(x), _ptr(y), _ptr(role), xmin, xmax, ymin, ymax,
+                                    kx, ky, float(delta), _ptr(tc), _ptr(vc))
+    if rc:
+        raise OracleError(rc, "partition")
+    toff = np.zeros(N + 1, np.int64)
+    voff = np.zeros(N + 1, np.int64)
+    np.cumsum(tc, out=toff[1:])
+    np.cumsum(vc, out=voff[1:])
+    tidx = np.empty(int(toff[-1]), np.int32)
+    vidx = np.empty(int(voff[-1]), np.int32)
+    rc = lib.oracle_partition_fill(n, _ptr(x), _ptr(y), _ptr(role), xmin, xmax, ymin, ymax,
+                                   kx, ky, float(delta), _ptr(toff), _ptr(tidx), _ptr(voff),
+                                   _ptr(vidx))
+    if rc:
+        raise OracleError(rc, "partition")
+    return Partition(toff, tidx, voff, vidx, kx, ky)
+
+
+def subset_cv(tx, ty, tv, vx, vy, vv, range_: float, sigma2: float, nugget: float,
+              long_double: bool = False) -> float:
+    """CV(y~_T, y_V, zeta) of Eq.4 with Eq.3's predictor for one
+    subset and one (range, sigma^2, nugget).  Raises OracleError(ENUMERIC) if not PD."""
+    lib = _load()
+    a = [np.ascontiguousarray(v, np.float64) for v in (tx, ty, tv, vx, vy, vv)]
+    out = np.zeros(1, np.float64)
+    f = lib.oracle_subset_cv_ld if long_double else lib.oracle_subset_cv
+    rc = f(a[0].shape[0], _ptr(a[0]), _ptr(a[1]), _ptr(a[2]), a[3].shape[0], _ptr(a[3]),
+           _ptr(a[4]), _ptr(a[5]), float(range_), float(sigma2), float(nugget), _ptr(out))
+    if rc:
+        raise OracleError(rc, "subset_cv")
+    return float(out[0])
+
+
+def neg2loglik(tx, ty, tv, range_: float, sigma2: float, nugget: float) -> float:
+    """-2 log-likelihood of Eq.2 for one training vector (NEXT row f3)."""
+    lib = _load()
+    a = [np.ascontiguousarray(v, np.float64) for v in (tx, ty, tv)]
+    out = np.zeros(1, np.float64)
+    rc = lib.oracle_neg2loglik(a[0].shape[0], _ptr(a[0]), _ptr(a[1]), _ptr(a[2]),
+                               float(range_), float(sigma2), float(nugget), _ptr(out))
+    if rc:
+        raise OracleError(rc, "neg2loglik")
+    return float(out[0])
+
+
+class CvReport:
+    """loss[c] = sum over subsets in ascending s (Alg.1 line 9; reading R13);
+    subset_loss[s, c]; status[c] = -1 ok else first subset whose factorization failed."""
+
+    def __init__(self, loss, subset_loss, status):
+        self.loss, self.subset_loss, self.status = loss, subset_loss, status
+
+
+def cv_loss(x, y, v, part: Partition, params, subsets=None, threads: int | None = None,
+            long_double: bool = False) -> CvReport:
+    """C~V of Eq.7 for each params row (range, sigma2, nugget), evaluated per
+    Algorithm 1: independent per-subset SSPE z_i, then z = sum z_i.
+
+    ``subsets`` restricts the evaluation to a sample (others left NaN and excluded from
+    the sum -- used only for bounded baselines and sampled parity).  The thread pool over
+    (subset, config) tasks is the parfor of Alg.1 line 4; it does not change any value.
+    """
+    params = np.asarray(params, np.float64).reshape(-1, 3)
+    C = params.shape[0]
+    N = part.n_subsets
+    sub = np.arange(N) if subsets is None else np.asarray(subsets, np.int64)
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    v = np.ascontiguousarray(v, np.float64)
+    res = np.full((N, C), np.nan)
+    st = np.zeros((N, C), np.int32)
+    k = part.k()
+    tasks = [(int(s), c) for s in sub for c in range(C)]
+    tasks.sort(key=lambda t: -int(k[t[0]]) ** 3)  # LPT order; does not change values
+
+    def run(t):
+        s, c = t
+        ti, vi = part.train(s), part.val(s)
+        try:
+            res[s, c] = subset_cv(x[ti], y[ti], v[ti], x[vi], y[vi], v[vi], *params[c],
+                                  long_double=long_double)
+        except OracleError as e:
+            if e.code != ENUMERIC:
+                raise
+            st[s, c] = 1
+
+    nthreads = threads or os.cpu_count() or 1
+    if nthreads == 1:
+        for t in tasks:
+            run(t)
+    else:
+        with ThreadPoolExecutor(nthreads) as ex:
+            list(ex.map(run, tasks))
+    loss = np.zeros(C)
+    status = np.full(C, -1, np.int32)
+    for c in range(C):
+        acc = 0.0
+        for s in sub:  # ascending subset order (Alg.1 line 9)
+            if st[s, c]:
+                if status[c] < 0:
+                    status[c] = s
+                continue
+            acc = acc + float(res[s, c])
+        loss[c] = math.nan if status[c] >= 0 else acc
+    return CvReport(loss, res, status)
+
+
+def subset_flops(k, m) -> float:
+    """Algorithmic flop count of one (subset, config) evaluation:
+    k^3/3 + k^2/2 + k/6 (Cholesky) + 2k^2 (two triangular solves) + 2mk + 3m."""
+    k = np.asarray(k, np.float64)
+    m = np.asarray(m, np.float64)
+    f = k ** 3 / 3 + k ** 2 / 2 + k / 6 + 2 * k ** 2 + 2 * m * k + 3 * m
+    return np.where(m > 0, f, 0.0)

@@ -1,0 +1,363 @@
+"""Pins for the CPU oracle (oracle/): each test checks it against something other than
+itself -- closed forms, values worked from the paper, library routines (numpy/scipy),
+exactness limits of Eq.7 and bit-exact metamorphic invariants -- chosen so that a dropped
+term, wrong sign/index or transposed operand anywhere in oracle.c fails one of them.
+
+Citations: P:n = PAPER.md line n (Gerber & Nychka, arXiv 1912.13132); R# = DESIGN.md reading.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg
+import scipy.stats
+
+import oracle
+import workloads
+
+
+def _cov(ax, ay, bx, by, theta):
+    d = np.sqrt((ax[:, None] - bx[None, :]) ** 2 + (ay[:, None] - by[None, :]) ** 2)
+    return np.exp(-d / theta)
+
+
+def _cv_numpy(tx, ty, tv, vx, vy, vv, theta, lam):
+    """Eq.4 with Eq.3 via LAPACK (scipy cho_factor/cho_solve): an independent library route."""
+    if len(vx) == 0:
+        return 0.0
+    if len(tx) == 0:
+        return float(np.sum(vv ** 2))
+    A = _cov(tx, ty, tx, ty, theta) + lam * np.eye(len(tx))
+    B = _cov(vx, vy, tx, ty, theta)
+    alpha = scipy.linalg.cho_solve(scipy.linalg.cho_factor(A, lower=True), tv)
+    e = B @ alpha - vv
+    return float(e @ e)
+
+
+# ----------------------------------------------------------------- closed forms (Eq.3)
+
+def test_exp_covariance_values(golden_dir):
+    """c(s1,s2,theta) = exp(-||s1-s2||/theta): a k=1 system with zero nugget
+    predicts c(v,t) * y_t exactly, so each golden covariance value is pinned."""
+    g = json.load(open(os.path.join(golden_dir, "closed_forms.json")))
+    for case in g["exp_cov"]:
+        t, v = case["s1"], case["s2"]
+        yv = 0.25
+        loss = oracle.subset_cv([t[0]], [t[1]], [1.0], [v[0]], [v[1]], [yv], case["theta"], 1.0, 0.0)
+        assert loss == pytest.approx((case["value"] - yv) ** 2, rel=1e-14)
+
+
+def test_kriging_k1_closed_form(golden_dir):
+    """n = 1: yhat = c(v,t) y_t / (1 + lambda), lambda = tau / sigma2."""
+    c = json.load(open(os.path.join(golden_dir, "closed_forms.json")))["k1"]
+    yv = -0.7
+    loss = oracle.subset_cv([c["t"][0]], [c["t"][1]], [c["y_t"]], [c["v"][0]], [c["v"][1]], [yv],
+                            c["range"], c["sigma2"], c["nugget"])
+    assert loss == pytest.approx((c["yhat"] - yv) ** 2, rel=1e-14)
+
+
+def test_kriging_k2_closed_form():
+    """k = 2: with a = 1+lambda, r = c(t1,t2), c_i = c(v,t_i):
+    yhat = [a(c1 y1 + c2 y2) - r(c1 y2 + c2 y1)] / (a^2 - r^2)  (2x2 inverse of Eq.3)."""
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        t = rng.uniform(0, 1, (2, 2))
+        v = rng.uniform(0, 1, 2)
+        y1, y2, yv = rng.standard_normal(3)
+        theta = rng.uniform(0.1, 1.0)
+        sigma2, nugget = rng.uniform(0.5, 2.0), rng.uniform(0.0, 0.5)
+        a = 1.0 + nugget / sigma2
+        r = math.exp(-math.dist(t[0], t[1]) / theta)
+        c1 = math.exp(-math.dist(v, t[0]) / theta)
+        c2 = math.exp(-math.dist(v, t[1]) / theta)
+        yhat = (a * (c1 * y1 + c2 * y2) - r * (c1 * y2 + c2 * y1)) / (a * a - r * r)
+        loss = oracle.subset_cv(t[:, 0], t[:, 1], [y1, y2], [v[0]], [v[1]], [yv], theta, sigma2, nugget)
+        assert loss == pytest.approx((yhat - yv) ** 2, rel=1e-11)
+
+
+def test_kriging_k3_adjugate_closed_form():
+    """k = 3: A = [[a,p,q],[p,a,s],[q,s,a]], det = a^3 + 2pqs - a(p^2+q^2+s^2),
+    adj = [[a^2-s^2, qs-ap, ps-aq], [qs-ap, a^2-q^2, pq-as], [ps-aq, pq-as, a^2-p^2]],
+    yhat = c^T adj y / det; two validation points (loss sums both, Eq.4)."""
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        t = rng.uniform(0, 1, (3, 2))
+        vs = rng.uniform(0, 1, (2, 2))
+        y = rng.standard_normal(3)
+        yv = rng.standard_normal(2)
+        theta = rng.uniform(0.1, 1.0)
+        sigma2, nugget = rng.uniform(0.5, 2.0), rng.uniform(0.01, 0.5)
+        a = 1.0 + nugget / sigma2
+        p = math.exp(-math.dist(t[0], t[1]) / theta)
+        q = math.exp(-math.dist(t[0], t[2]) / theta)
+        s = math.exp(-math.dist(t[1], t[2]) / theta)
+        det = a ** 3 + 2 * p * q * s - a * (p * p + q * q + s * s)
+        adj = np.array([[a * a - s * s, q * s - a * p, p * s - a * q],
+                        [q * s - a * p, a * a - q * q, p * q - a * s],
+                        [p * s - a * q, p * q - a * s, a * a - p * p]])
+        expected = 0.0
+        for i in range(2):
+            cvec = np.array([math.exp(-math.dist(vs[i], t[j]) / theta) for j in range(3)])
+            e = cvec @ adj @ y / det - yv[i]
+            expected += e * e
+        loss = oracle.subset_cv(t[:, 0], t[:, 1], y, vs[:, 0], vs[:, 1], yv, theta, sigma2, nugget)
+        assert loss == pytest.approx(expected, rel=1e-10)
+
+
+def test_interpolation_at_observed_sites_zero_nugget():
+    """tau = 0: the kriging predictor interpolates, yhat(t_j) = y_j (Eq.3 with lambda = 0)."""
+    rng = np.random.default_rng(3)
+    k = 40
+    t = rng.uniform(0, 1, (k, 2))
+    y = rng.standard_normal(k)
+    for j in (0, 17, 39):
+        # validation value y_j + 1 at the site of t_j: the error is exactly 1 when yhat = y_j
+        loss = oracle.subset_cv(t[:, 0], t[:, 1], y, [t[j, 0]], [t[j, 1]], [y[j] + 1.0], 0.2, 1.0, 0.0)
+        assert loss == pytest.approx(1.0, abs=1e-9)
+
+
+def test_far_field_predicts_zero():
+    """Validation >= 50 theta from every training point: yhat = 0 (zero-mean prior, Eq.1)."""
+    rng = np.random.default_rng(5)
+    t = rng.uniform(0, 1, (30, 2))
+    y = rng.standard_normal(30)
+    theta = 0.02
+    vx, vy, vv = [1.0 + 50 * theta, 3.0], [1.0 + 50 * theta, 2.0], [0.4, -1.3]
+    loss = oracle.subset_cv(t[:, 0], t[:, 1], y, vx, vy, vv, theta, 1.0, 0.1)
+    assert loss == pytest.approx(0.4 ** 2 + 1.3 ** 2, rel=1e-10)
+
+
+def test_degenerate_subsets():
+    """R10: m = 0 -> loss exactly 0; R11: k = 0 -> yhat = 0, loss = sum y_V^2."""
+    assert oracle.subset_cv([0.1], [0.2], [1.0], [], [], [], 0.3, 1.0, 0.1) == 0.0
+    assert oracle.subset_cv([], [], [], [0.5, 0.2], [0.5, 0.1], [2.0, -3.0], 0.3, 1.0, 0.1) == 13.0
+    assert oracle.subset_cv([], [], [], [], [], [], 0.3, 1.0, 0.1) == 0.0
+
+
+def test_non_positive_definite_is_reported():
+    """R12: duplicate sites with zero nugget make Sigma singular -> ENUMERIC (no jitter)."""
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.subset_cv([0.3, 0.3], [0.4, 0.4], [1.0, 2.0], [0.5], [0.5], [0.0], 0.5, 1.0, 0.0)
+    assert ei.value.code == oracle.ENUMERIC
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.subset_cv([0.3], [0.4], [1.0], [0.5], [0.5], [0.0], -1.0, 1.0, 0.0)
+    assert ei.value.code == oracle.EINVAL
+
+
+def test_matches_lapack_cho_solve():
+    """Special case that reduces to a library routine: Eq.3 + Eq.4 via scipy's LAPACK
+    Cholesky solve (k = 120, m = 15) agrees to 1e-12 relative."""
+    rng = np.random.default_rng(19)
+    for theta, sigma2, nugget in ((0.1, 1.0, 0.1), (0.5, 2.0, 0.05), (0.03, 0.7, 0.3)):
+        t = rng.uniform(0, 1, (120, 2))
+        v = rng.uniform(0, 1, (15, 2))
+        y = rng.standard_normal(120)
+        yv = rng.standard_normal(15)
+        lo = oracle.subset_cv(t[:, 0], t[:, 1], y, v[:, 0], v[:, 1], yv, theta, sigma2, nugget)
+        ref = _cv_numpy(t[:, 0], t[:, 1], y, v[:, 0], v[:, 1], yv, theta, nugget / sigma2)
+        assert lo == pytest.approx(ref, rel=1e-12)
+
+
+def test_long_double_variant_agrees():
+    rng = np.random.default_rng(23)
+    t = rng.uniform(0, 1, (200, 2))
+    v = rng.uniform(0, 1, (20, 2))
+    y = rng.standard_normal(200)
+    yv = rng.standard_normal(20)
+    a = oracle.subset_cv(t[:, 0], t[:, 1], y, v[:, 0], v[:, 1], yv, 0.2, 1.0, 0.1)
+    b = oracle.subset_cv(t[:, 0], t[:, 1], y, v[:, 0], v[:, 1], yv, 0.2, 1.0, 0.1, long_double=True)
+    assert a == pytest.approx(b, rel=1e-11)
+
+
+# ------------------------------------------------------------- -2 log-likelihood (Eq.2)
+
+def test_neg2loglik_closed_form_and_library():
+    """Eq.2: n = 1 -> log 2pi + log(sigma2 + tau) + y^2/(sigma2 + tau);
+    n = 50 -> -2 * scipy multivariate_normal.logpdf."""
+    got = oracle.neg2loglik([0.2], [0.3], [1.5], 0.4, 2.0, 0.5)
+    assert got == pytest.approx(math.log(2 * math.pi) + math.log(2.5) + 1.5 ** 2 / 2.5, rel=1e-14)
+    rng = np.random.default_rng(29)
+    t = rng.uniform(0, 1, (50, 2))
+    y = rng.standard_normal(50)
+    cov = 1.3 * _cov(t[:, 0], t[:, 1], t[:, 0], t[:, 1], 0.25) + 0.2 * np.eye(50)
+    ref = -2 * scipy.stats.multivariate_normal(np.zeros(50), cov).logpdf(y)
+    assert oracle.neg2loglik(t[:, 0], t[:, 1], y, 0.25, 1.3, 0.2) == pytest.approx(ref, rel=1e-11)
+
+
+# --------------------------------------------------------------------- partition pins
+
+def test_golden_partition(golden_dir):
+    """Hand-worked membership (tests/golden/partition_small.json)."""
+    g = json.load(open(os.path.join(golden_dir, "partition_small.json")))
+    pts = np.array(g["points"])
+    part = oracle.partition(pts[:, 0], pts[:, 1], pts[:, 2].astype(np.uint8), g["domain"],
+                            g["kx"], g["ky"], g["delta"])
+    for s in range(4):
+        assert part.train(s).tolist() == g["train"][s]
+        assert part.val(s).tolist() == g["val"][s]
+
+
+def test_edges_rule():
+    """R4: e_i = a + i*w with w = (b-a)/K, e_K = b exactly."""
+    e = oracle.edges(0.0, 50.0, 50)
+    assert e[-1] == 50.0 and e[0] == 0.0
+    assert all(e[i] == 0.0 + i * 1.0 for i in range(50))
+    e = oracle.edges(0.0, 1.0, 3)
+    assert e.tolist() == [0.0, 1.0 / 3.0, 2 * (1.0 / 3.0), 1.0]
+
+
+def _independent_membership(x, y, role, domain, kx, ky, delta):
+    """Vectorised numpy membership by the same readings (R2-R6), as sets."""
+    xmin, xmax, ymin, ymax = domain
+    ex = np.array([xmin + i * ((xmax - xmin) / kx) for i in range(kx)] + [xmax])
+    ey = np.array([ymin + i * ((ymax - ymin) / ky) for i in range(ky)] + [ymax])
+    cx = np.clip(np.searchsorted(ex, x, side="right") - 1, 0, kx - 1)
+    cy = np.clip(np.searchsorted(ey, y, side="right") - 1, 0, ky - 1)
+    train, val = [], []
+    for s in range(kx * ky):
+        ix, iy = s % kx, s // kx
+        hx = np.inf if ix == kx - 1 else ex[ix + 1] + delta
+        hy = np.inf if iy == ky - 1 else ey[iy + 1] + delta
+        inx = (ex[ix] - delta <= x) & (x < hx)
+        iny = (ey[iy] - delta <= y) & (y < hy)
+        train.append(np.nonzero((role == 0) & inx & iny)[0])
+        val.append(np.nonzero((role == 1) & (cx == ix) & (cy == iy))[0])
+    return train, val
+
+
+@pytest.mark.parametrize("delta", [0.0, 0.02, 0.13])
+def test_partition_invariants(delta):
+    """Sum m = n_V without duplicates; delta = 0 training lists partition y_T; lists are
+    ascending; equal to an independent vectorised membership; deterministic."""
+    x, y, v, role = workloads.random_points(31, 3000, frac_val=0.1, frac_test=0.1)
+    dom = (0.0, 1.0, 0.0, 1.0)
+    part = oracle.partition(x, y, role, dom, 7, 5, delta)
+    assert part.m().sum() == (role == 1).sum()
+    assert np.array_equal(np.sort(part.val_idx), np.nonzero(role == 1)[0])
+    for s in range(part.n_subsets):
+        assert np.all(np.diff(part.train(s)) > 0) and np.all(np.diff(part.val(s)) > 0)
+    if delta == 0.0:
+        assert np.array_equal(np.sort(part.train_idx), np.nonzero(role == 0)[0])
+    tr, va = _independent_membership(x, y, role, dom, 7, 5, delta)
+    for s in range(part.n_subsets):
+        assert np.array_equal(part.train(s), tr[s]) and np.array_equal(part.val(s), va[s])
+    again = oracle.partition(x, y, role, dom, 7, 5, delta)
+    assert np.array_equal(again.train_idx, part.train_idx) and np.array_equal(again.train_off, part.train_off)
+
+
+def test_partition_nesting():
+    """delta1 <= delta2 -> every training list for delta1 is a subset of delta2's."""
+    x, y, v, role = workloads.random_points(37, 2000)
+    a = oracle.partition(x, y, role, (0, 1, 0, 1), 4, 4, 0.01)
+    b = oracle.partition(x, y, role, (0, 1, 0, 1), 4, 4, 0.05)
+    for s in range(16):
+        assert set(a.train(s).tolist()) <= set(b.train(s).tolist())
+        assert np.array_equal(a.val(s), b.val(s))
+
+
+def test_partition_rejects_bad_input():
+    x, y, v, role = workloads.random_points(41, 50)
+    with pytest.raises(oracle.OracleError):
+        oracle.partition(x + 2.0, y, role, (0, 1, 0, 1), 2, 2, 0.1)  # outside D
+    with pytest.raises(oracle.OracleError):
+        oracle.partition(x, y, role, (0, 1, 0, 1), 0, 2, 0.1)  # kx < 1
+    with pytest.raises(oracle.OracleError):
+        oracle.partition(x, y, role, (0, 1, 0, 1), 2, 2, -0.1)  # delta < 0
+
+
+# -------------------------------------------------------------- Eq.7 exactness limits
+
+def _setup(seed=43, n=600):
+    x, y, v, role = workloads.random_points(seed, n, frac_val=0.15)
+    return x, y, v, role
+
+
+def test_single_subset_reproduces_global_cv():
+    """N = 1 (one tile): Eq.7 reduces to Eq.4 over all data."""
+    x, y, v, role = _setup()
+    part = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
+    t, w = role == 0, role == 1
+    for theta, s2, tau in ((0.1, 1.0, 0.1), (0.3, 2.0, 0.05)):
+        rep = oracle.cv_loss(x, y, v, part, [[theta, s2, tau]], threads=1)
+        ref = _cv_numpy(x[t], y[t], v[t], x[w], y[w], v[w], theta, tau / s2)
+        assert rep.loss[0] == pytest.approx(ref, rel=1e-11)
+
+
+def test_delta_saturating_domain_reproduces_global_cv():
+    """A shell wider than D makes every y~^i_T the whole y_T: sum_i CV_i = CV."""
+    x, y, v, role = _setup()
+    part = oracle.partition(x, y, role, (0, 1, 0, 1), 3, 2, 1.5)
+    assert all(part.k() == (role == 0).sum())
+    one = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
+    p = [[0.15, 1.0, 0.1]]
+    a = oracle.cv_loss(x, y, v, part, p, threads=2).loss[0]
+    b = oracle.cv_loss(x, y, v, one, p, threads=1).loss[0]
+    assert a == pytest.approx(b, rel=1e-12)
+    t, w = role == 0, role == 1
+    assert a == pytest.approx(_cv_numpy(x[t], y[t], v[t], x[w], y[w], v[w], 0.15, 0.1), rel=1e-11)
+
+
+def test_delta_zero_is_sum_of_independent_tile_cvs():
+    """delta = 0: Eq.5 generalised -- each tile's own training predicts its own validation
+    (P:144-151); checked per subset against LAPACK on independently selected tiles."""
+    x, y, v, role = _setup(47, 900)
+    part = oracle.partition(x, y, role, (0, 1, 0, 1), 3, 3, 0.0)
+    tr, va = _independent_membership(x, y, role, (0, 1, 0, 1), 3, 3, 0.0)
+    rep = oracle.cv_loss(x, y, v, part, [[0.2, 1.0, 0.1]], threads=2)
+    total = 0.0
+    for s in range(9):
+        ref = _cv_numpy(x[tr[s]], y[tr[s]], v[tr[s]], x[va[s]], y[va[s]], v[va[s]], 0.2, 0.1)
+        assert rep.subset_loss[s, 0] == pytest.approx(ref, rel=1e-11)
+        total += ref
+    assert rep.loss[0] == pytest.approx(total, rel=1e-12)
+
+
+# ------------------------------------------------------ bit-exact metamorphic invariants
+
+def test_power_of_two_invariants_bit_exact():
+    """(2 sigma2, 2 tau) leaves lambda bit-identical (R8) -> identical loss; y -> 2y scales
+    every op by 2 exactly -> loss x4 exactly; (x, y, D, delta, theta) x2 -> identical
+    membership and loss (sqrt(4s) = 2 sqrt(s) under correct rounding)."""
+    x, y, v, role = _setup(53, 800)
+    dom = (0.0, 1.0, 0.0, 1.0)
+    part = oracle.partition(x, y, role, dom, 2, 2, 0.1)
+    base = oracle.cv_loss(x, y, v, part, [[0.2, 1.0, 0.1]], threads=2)
+    sc = oracle.cv_loss(x, y, v, part, [[0.2, 2.0, 0.2]], threads=2)
+    assert np.array_equal(base.subset_loss, sc.subset_loss)
+    vv = oracle.cv_loss(x, y, 2 * v, part, [[0.2, 1.0, 0.1]], threads=2)
+    assert np.array_equal(vv.subset_loss, 4 * base.subset_loss)
+    part2 = oracle.partition(2 * x, 2 * y, role, (0.0, 2.0, 0.0, 2.0), 2, 2, 0.2)
+    assert np.array_equal(part2.train_idx, part.train_idx) and np.array_equal(part2.val_idx, part.val_idx)
+    cc = oracle.cv_loss(2 * x, 2 * y, v, part2, [[0.4, 1.0, 0.1]], threads=2)
+    assert np.array_equal(cc.subset_loss, base.subset_loss)
+
+
+def test_permutation_invariance():
+    """Permuting the input order permutes member indices; losses agree to 1e-12."""
+    x, y, v, role = _setup(59, 700)
+    perm = np.random.default_rng(1).permutation(x.size)
+    inv = np.argsort(perm)
+    a = oracle.partition(x, y, role, (0, 1, 0, 1), 3, 2, 0.08)
+    b = oracle.partition(x[perm], y[perm], role[perm], (0, 1, 0, 1), 3, 2, 0.08)
+    for s in range(6):
+        assert set(a.train(s).tolist()) == set(perm[b.train(s)].tolist())
+        assert set(a.val(s).tolist()) == set(perm[b.val(s)].tolist())
+    pa = oracle.cv_loss(x, y, v, a, [[0.1, 1.0, 0.1]], threads=2)
+    pb = oracle.cv_loss(x[perm], y[perm], v[perm], b, [[0.1, 1.0, 0.1]], threads=2)
+    np.testing.assert_allclose(pb.subset_loss, pa.subset_loss, rtol=1e-12)
+    assert inv.size == x.size
+
+
+def test_status_reports_first_failing_subset():
+    """R12 / SPEC S:422: a non-PD subset makes loss[c] NaN and status[c] its id; other
+    configs are unaffected."""
+    x = np.array([0.1, 0.1, 0.2, 0.8, 0.9, 0.85])
+    y = np.array([0.1, 0.1, 0.3, 0.8, 0.7, 0.9])
+    v = np.array([1.0, 2.0, 0.5, 0.3, -0.2, 0.4])
+    role = np.array([0, 0, 1, 0, 0, 1], np.uint8)
+    part = oracle.partition(x, y, role, (0, 1, 0, 1), 2, 1, 0.0)
+    rep = oracle.cv_loss(x, y, v, part, [[0.2, 1.0, 0.0], [0.2, 1.0, 0.1]], threads=1)
+    assert math.isnan(rep.loss[0]) and rep.status[0] == 0
+    assert rep.status[1] == -1 and np.isfinite(rep.loss[1])

@@ -1,0 +1,215 @@
+"""Seeded synthetic workloads c1..c5 (BASELINE.json ``configs``).
+
+Shared by the oracle side (tests, cpu baseline) and the CUDA side (tests, bench, smoke).
+This module holds NONE of the method's arithmetic: it only draws locations, simulates a
+Gaussian field to be cross-validated, assigns roles and lays out the parameter grid.
+Random numbers come from numpy ``Generator(PCG64)`` with seeds 1001..1005 and independent
+``SeedSequence.spawn`` streams; the field sum is evaluated with torch (CPU or CUDA) in
+fp64 because c4/c5 need 1.6e10 / 8.2e10 cosines.  Whatever device evaluates the field,
+both implementations then consume the SAME arrays within a run.
+
+Stand-in statement: the paper's measured data (5M LiDAR canopy-height residuals,
+PAPER.md P:339-358, and the 20,000-residual subset of P:394) are not available; c5 and c2
+are synthetic stand-ins with the paper's sizes, split fractions,
+irregular spacing (jittered lattice with dropouts) and exponential model.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+TRAIN, VALIDATION, TEST = 0, 1, 2
+
+
+@dataclass
+class Workload:
+    name: str
+    x: np.ndarray            # float64 [n]
+    y: np.ndarray            # float64 [n]
+    value: np.ndarray        # float64 [n]
+    role: np.ndarray         # uint8 [n]: 0 train, 1 validation, 2 test
+    domain: tuple            # (xmin, xmax, ymin, ymax)
+    kx: int
+    ky: int
+    delta: float
+    params: np.ndarray       # float64 [C, 3] rows (range, sigma2, nugget)
+    truth: tuple = field(default=(1.0, 1.0, 0.1))
+
+    @property
+    def n(self) -> int:
+        return int(self.x.shape[0])
+
+
+@dataclass(frozen=True)
+class Spec:
+    name: str
+    seed: int
+    n: int
+    domain: tuple
+    layout: str            # "uniform" | "clustered" | "lattice"
+    field: str             # "exact" | "rff"
+    rff_m: int
+    sigma2: float
+    theta: float
+    tau: float
+    kx: int
+    ky: int
+    delta: float
+    split: tuple           # (train, validation) fractions; rest is test
+    grid: tuple            # ((lo, hi, count) for range, sigma2, nugget)
+
+
+SPECS = {
+    "c1": Spec("c1", 1001, 2_000, (0.0, 1.0, 0.0, 1.0), "uniform", "exact", 0, 1.0, 0.1, 0.1,
+               2, 2, 0.05, (0.9, 0.1), ((0.1, 0.1, 1), (1.0, 1.0, 1), (0.1, 0.1, 1))),
+    "c2": Spec("c2", 1002, 20_000, (0.0, 1.0, 0.0, 1.0), "uniform", "rff", 4_096, 1.0, 0.1, 0.1,
+               10, 10, 0.02, (0.9, 0.1), ((0.02, 0.2, 5), (0.5, 2.0, 5), (0.05, 0.2, 3))),
+    "c3": Spec("c3", 1003, 200_000, (0.0, 10.0, 0.0, 10.0), "uniform", "rff", 8_192, 1.0, 0.3, 0.1,
+               40, 40, 0.1, (0.9, 0.1), ((0.15, 0.6, 3), (0.5, 2.0, 3), (0.05, 0.2, 3))),
+    "c4": Spec("c4", 1004, 1_000_000, (0.0, 20.0, 0.0, 20.0), "clustered", "rff", 16_384, 1.0, 0.5,
+               0.05, 100, 100, 0.15, (0.8, 0.1), ((0.25, 1.0, 4), (0.5, 2.0, 4), (0.025, 0.1, 4))),
+    "c5": Spec("c5", 1005, 5_000_000, (0.0, 50.0, 0.0, 50.0), "lattice", "rff", 16_384, 1.0, 1.0, 0.1,
+               50, 50, 0.3, (0.8, 0.1), ((0.5, 2.0, 5), (0.5, 2.0, 5), (0.05, 0.2, 5))),
+}
+
+
+def geometric(lo: float, hi: float, count: int) -> np.ndarray:
+    """Geometric grid (SPEC S:484 style)."""
+    if count == 1:
+        return np.array([lo], np.float64)
+    return lo * (hi / lo) ** (np.arange(count, dtype=np.float64) / (count - 1))
+
+
+def param_grid(spec: Spec) -> np.ndarray:
+    """(range, sigma2, nugget) rows, range outermost, nugget innermost (Appendix B #6)."""
+    r, s, t = (geometric(*g) for g in spec.grid)
+    rows = [(a, b, c) for a in r for b in s for c in t]
+    return np.array(rows, np.float64).reshape(-1, 3)
+
+
+def _locations(spec: Spec, rng: np.random.Generator):
+    xmin, xmax, ymin, ymax = spec.domain
+    n = spec.n
+    if spec.layout == "uniform":
+        x = rng.uniform(xmin, xmax, n)
+        y = rng.uniform(ymin, ymax, n)
+    elif spec.layout == "clustered":
+        # 50 % uniform background + 50 % from 200 equal-weight isotropic Gaussian clusters
+        # (sd 0.5); out-of-domain draws are redrawn (Appendix B #7).
+        nb = n // 2
+        nc = n - nb
+        xb = rng.uniform(xmin, xmax, nb)
+        yb = rng.uniform(ymin, ymax, nb)
+        cx = rng.uniform(xmin, xmax, 200)
+        cy = rng.uniform(ymin, ymax, 200)
+        lab = rng.integers(0, 200, nc)
+        xc = cx[lab] + 0.5 * rng.standard_normal(nc)
+        yc = cy[lab] + 0.5 * rng.standard_normal(nc)
+        bad = (xc < xmin) | (xc > xmax) | (yc < ymin) | (yc > ymax)
+        while bad.any():
+            idx = np.nonzero(bad)[0]
+            xc[idx] = cx[lab[idx]] + 0.5 * rng.standard_normal(idx.size)
+            yc[idx] = cy[lab[idx]] + 0.5 * rng.standard_normal(idx.size)
+            bad = (xc < xmin) | (xc > xmax) | (yc < ymin) | (yc > ymax)
+        x = np.concatenate([xb, xc])
+        y = np.concatenate([yb, yc])
+    elif spec.layout == "lattice":
+        # 2,500 x 2,500 lattice with spacing h = 0.02 on [0,50]^2; exactly n sites kept by a
+        # seeded choice (20 % dropout); each kept site jittered by U(-1/4, 1/4) h per axis.
+        side = 2_500
+        h = (xmax - xmin) / side
+        keep = np.sort(rng.choice(side * side, size=n, replace=False))
+        i = (keep % side).astype(np.float64)
+        j = (keep // side).astype(np.float64)
+        x = xmin + ((i + 0.5) + rng.uniform(-0.25, 0.25, n)) * h
+        y = ymin + ((j + 0.5) + rng.uniform(-0.25, 0.25, n)) * h
+    else:
+        raise ValueError(spec.layout)
+    return np.ascontiguousarray(x), np.ascontiguousarray(y)
+
+
+def _field_exact(spec: Spec, x, y, rng: np.random.Generator) -> np.ndarray:
+    """Exact simulation y = chol(sigma2 Sigma(theta) + tau I) z (Eq.1), small n."""
+    d = np.sqrt((x[:, None] - x[None, :]) ** 2 + (y[:, None] - y[None, :]) ** 2)
+    cov = spec.sigma2 * np.exp(-d / spec.theta) + spec.tau * np.eye(x.size)
+    chol = np.linalg.cholesky(cov)
+    return chol @ rng.standard_normal(x.size)
+
+
+def _field_rff(spec: Spec, x, y, rng: np.random.Generator, device: str) -> np.ndarray:
+    """Random Fourier features for exp(-||h||/theta) in 2-D: omega = g / (theta |u|) with
+    g ~ N(0, I2), u ~ N(0, 1) (bivariate Cauchy, the exact spectral density), phases
+    U[0, 2pi); f = sqrt(2 sigma2 / M) sum cos(omega.s + b); y = f + sqrt(tau) eps."""
+    import torch
+
+    M = spec.rff_m
+    g = rng.standard_normal((M, 2))
+    u = rng.standard_normal(M)
+    omega = g / (spec.theta * np.abs(u))[:, None]
+    b = rng.uniform(0.0, 2.0 * math.pi, M)
+    eps = rng.standard_normal(x.size)
+    dev = torch.device(device)
+    om = torch.as_tensor(omega, dtype=torch.float64, device=dev)
+    bb = torch.as_tensor(b, dtype=torch.float64, device=dev)
+    out = np.empty(x.size, np.float64)
+    chunk = 1 << 14 if dev.type == "cuda" else 1 << 11
+    scale = math.sqrt(2.0 * spec.sigma2 / M)
+    for s0 in range(0, x.size, chunk):
+        s1 = min(x.size, s0 + chunk)
+        xs = torch.as_tensor(x[s0:s1], dtype=torch.float64, device=dev)
+        ys = torch.as_tensor(y[s0:s1], dtype=torch.float64, device=dev)
+        ph = xs[:, None] * om[None, :, 0] + ys[:, None] * om[None, :, 1] + bb[None, :]
+        out[s0:s1] = (torch.cos(ph).sum(dim=1) * scale).cpu().numpy()
+    return out + math.sqrt(spec.tau) * eps
+
+
+def _roles(spec: Spec, rng: np.random.Generator) -> np.ndarray:
+    """One seeded permutation: first n_T train, next n_V validation, rest test (R7)."""
+    n = spec.n
+    nt = int(round(spec.split[0] * n))
+    nv = int(round(spec.split[1] * n))
+    perm = rng.permutation(n)
+    role = np.full(n, TEST, np.uint8)
+    role[perm[:nt]] = TRAIN
+    role[perm[nt:nt + nv]] = VALIDATION
+    return role
+
+
+def make(name: str, device: str = "cpu", n: int | None = None) -> Workload:
+    """Generate workload ``name`` (c1..c5).  ``n`` overrides the size for reduced test
+    variants (same layout/field/tiles/grid; the name gets a suffix)."""
+    spec = SPECS[name]
+    if n is not None and n != spec.n:
+        if spec.layout == "lattice":
+            raise ValueError("lattice layout has a fixed size")
+        spec = Spec(**{**spec.__dict__, "name": f"{name}_n{n}", "n": n})
+    ss = np.random.SeedSequence(spec.seed)
+    s_loc, s_field, s_role = ss.spawn(3)
+    x, y = _locations(spec, np.random.Generator(np.random.PCG64(s_loc)))
+    frng = np.random.Generator(np.random.PCG64(s_field))
+    if spec.field == "exact":
+        v = _field_exact(spec, x, y, frng)
+    else:
+        v = _field_rff(spec, x, y, frng, device)
+    role = _roles(spec, np.random.Generator(np.random.PCG64(s_role)))
+    return Workload(spec.name, x, y, np.ascontiguousarray(v), role, spec.domain, spec.kx, spec.ky,
+                    spec.delta, param_grid(spec), (spec.theta, spec.sigma2, spec.tau))
+
+
+def random_points(seed: int, n: int, domain=(0.0, 1.0, 0.0, 1.0), frac_val: float = 0.1,
+                  frac_test: float = 0.0):
+    """Small seeded i.i.d. inputs for unit and edge-case tests (values ~ N(0,1))."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    xmin, xmax, ymin, ymax = domain
+    x = rng.uniform(xmin, xmax, n)
+    y = rng.uniform(ymin, ymax, n)
+    v = rng.standard_normal(n)
+    role = np.zeros(n, np.uint8)
+    perm = rng.permutation(n)
+    nv = int(round(frac_val * n))
+    nt = int(round(frac_test * n))
+    role[perm[:nv]] = VALIDATION
+    role[perm[nv:nv + nt]] = TEST
+    return x, y, v, role
