@@ -1,0 +1,197 @@
+/*
+ * pgpcv.h -- C ABI of libpgpcv: the data-parallel hot path of parallel cross-validation
+ * for Gaussian-process models (Gerber & Nychka, "Parallel cross-validation: a scalable
+ * fitting method for Gaussian process models", arXiv 1912.13132) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n (LaTeX source of the paper); R# = reading number in
+ * DESIGN.md (where the paper is silent, the reading taken).
+ *
+ * The library evaluates, for every parameter configuration zeta = (range, sigma2, nugget),
+ *
+ *     C~V(y_T, y_V, zeta) = sum_{i=1..N} CV(y~^i_T, y^i_V, zeta)                 Eq.7
+ *     CV(y_T, y_V, zeta)  = sum_v (yhat_v - y_v)^2                                Eq.4
+ *     yhat_p = Sigma_p^T (Sigma + lambda I)^{-1} y,  lambda = nugget / sigma2    Eq.3
+ *     Sigma_ij = exp(-||s_i - s_j|| / range)                                      Sec.3
+ *
+ * as Algorithm 1 does: the data are divided into subsets once
+ * (pgpcv_partition, Alg.1 lines 2-3), each subset's local SSPE z_i is computed
+ * (pgpcv_cv_loss, lines 4-8) and the z_i are combined (line 9; across GPUs by one NCCL
+ * all-reduce after pgpcv_shard).
+ *
+ * Conventions for every entry point:
+ *   - Return value: PGPCV_OK (0) or a negative PGPCV_E* code; no exception or abort
+ *     crosses the ABI.  pgpcv_last_error(ctx) returns a message for the last failure.
+ *   - Host pointers are caller-owned and only read/written for the duration of the call
+ *     (the library copies in/out).  Device pointers (the *_device variants) must be
+ *     memory of the ctx's CUDA device and stay valid for the duration of the call.
+ *   - A ctx owns all of its device memory, its CUDA stream and its NCCL communicator.
+ *     One ctx per process per GPU; a ctx is not thread-safe.
+ *   - Floating point is IEEE binary64 throughout (the paper's R arithmetic).
+ */
+#ifndef PGPCV_H
+#define PGPCV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGPCV_VERSION 1
+
+/* Error codes. */
+#define PGPCV_OK 0
+#define PGPCV_EINVAL (-2)   /* NaN/Inf input, point outside domain, range<=0, sigma2<=0,
+                               nugget<0, delta<0, kx or ky < 1, n >= 2^31, bad role byte,
+                               a subset larger than PGPCV_MAX_K, NULL where required */
+#define PGPCV_ENUMERIC (-3) /* some (subset, config) was not positive definite (a pivot <= 0
+                               or NaN in the Cholesky, R12): loss[c] = NaN and status[c] = the
+                               first such subset; all other configs are valid */
+#define PGPCV_EEMPTY (-4)   /* every subset lacks validation data: the loss is undefined */
+#define PGPCV_ECUDA (-5)    /* CUDA runtime or launch failure */
+#define PGPCV_ENOMEM (-6)   /* device or host allocation failed */
+#define PGPCV_ENCCL (-7)    /* NCCL unavailable or a collective failed */
+#define PGPCV_ESTATE (-8)   /* cv_loss before partition, or shard after cv_loss */
+
+/* Largest training subset one factorization slot supports (shared-memory bound of the
+ * back-substitution; a 19,200-point subset already needs a 2.9 GB factor). */
+#define PGPCV_MAX_K 19200
+
+/* Point roles (R7): 0 = training (y_T), 1 = validation (y_V), 2 = test (ignored). */
+#define PGPCV_ROLE_TRAIN 0
+#define PGPCV_ROLE_VALIDATION 1
+#define PGPCV_ROLE_TEST 2
+
+typedef struct pgpcv_ctx pgpcv_ctx; /* opaque */
+
+/* Rectangular domain D: [xmin, xmax] x [ymin, ymax]; tiles are half-open
+ * with the domain's top edges closed (R3). */
+typedef struct {
+    double xmin, xmax, ymin, ymax;
+} pgpcv_rect;
+
+/* One covariance configuration in BASELINE order; only lambda = nugget / sigma2 and
+ * range enter the prediction (R8). range > 0, sigma2 > 0, nugget >= 0. */
+typedef struct {
+    double range, sigma2, nugget;
+} pgpcv_param;
+
+/* Summary of a partition (sizes of Alg.1's y~^i_T and y^i_V). */
+typedef struct {
+    int64_t n_subsets;   /* N = kx * ky */
+    int64_t sum_k;       /* total training memberships, sum_i |y~^i_T| */
+    int64_t sum_m;       /* total validation memberships, sum_i |y^i_V| (= n_V) */
+    int64_t max_k;       /* largest training subset (the paper's k) */
+    int64_t max_m;       /* largest validation subset */
+    int64_t n_empty_val; /* subsets with no validation data (loss 0, "ignored") */
+    int64_t n_train;     /* points with role 0 */
+    int64_t n_val;       /* points with role 1 */
+} pgpcv_partition_info;
+
+/* Device-side timing of the last pgpcv_cv_loss call (CUDA events on the ctx stream). */
+typedef struct {
+    double kernel_ms;     /* the dominant kernel (batched Cholesky/solve/predict) */
+    double total_ms;      /* whole call: kernels + reduction + collective + result copy */
+    double flops;         /* algorithmic FP64 flops this rank executed */
+    int64_t n_evals;      /* (subset, config) evaluations this rank executed (m > 0 only) */
+    int32_t launches;     /* number of libpgpcv kernel launches in the call */
+    int32_t n_slots;      /* resident CTAs (factorization slots) of the dominant kernel */
+} pgpcv_timing;
+
+/* Library version (PGPCV_VERSION).  Never fails; needs no GPU. */
+int pgpcv_version(void);
+
+/* Create a context on CUDA device `cuda_device` (>= 0).  Creates a non-blocking stream.
+ * *out receives the handle (NULL on failure).  Errors: EINVAL (bad device / NULL out),
+ * ECUDA (no device or no sm_100 device), ENOMEM. */
+int pgpcv_create(int cuda_device, pgpcv_ctx **out);
+
+/* Release every device buffer, the stream (if owned) and the NCCL communicator.  NULL is
+ * a no-op. */
+void pgpcv_destroy(pgpcv_ctx *ctx);
+
+/* Message for the last non-zero return on ctx ("" if none).  Owned by ctx; valid until
+ * the next call on ctx.  ctx == NULL returns the message of the last failed
+ * pgpcv_create. */
+const char *pgpcv_last_error(const pgpcv_ctx *ctx);
+
+/* Use `stream` (a cudaStream_t of the ctx device, e.g. torch's current stream) for all
+ * later work; NULL restores the ctx's own stream.  The caller keeps ownership. */
+int pgpcv_set_stream(pgpcv_ctx *ctx, void *stream);
+
+/* Alg.1 lines 2-3, once per dataset: divide the n points into N = kx*ky
+ * subsets (R1: equal tiles).  Subset s = iy*kx + ix (R5).
+ *   training list  y~^s_T = {p : role[p] = 0 and p in the tile's L-inf dilation by
+ *                            delta, clipped to D}          (shell; R2, R3, R4)
+ *   validation list y^s_V = {p : role[p] = 1 and p in the core tile}    (Eq.7; R6)
+ * Both lists are in ascending point index.  Membership is decided by exact FP64
+ * comparisons against tile edges e_i = xmin + i*w (w = (xmax-xmin)/kx, no FMA, e_kx =
+ * xmax) and dilated bounds e_i - delta, e_{i+1} + delta; it is bit-exact and identical on
+ * every rank.  The member coordinates/values are then staged subset-contiguously in HBM,
+ * where they stay for every later pgpcv_cv_loss call.
+ *   x, y, value: float64[n] host arrays (SoA); role: uint8[n] host array.
+ *   info_out: may be NULL.
+ * Replaces any previous partition.  Errors: EINVAL, ECUDA, ENOMEM. */
+int pgpcv_partition(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y,
+                    const double *value, const uint8_t *role, pgpcv_rect domain, int32_t kx,
+                    int32_t ky, double delta, pgpcv_partition_info *info_out);
+
+/* Same as pgpcv_partition with x, y, value, role already in device memory of the ctx
+ * device (no host-to-device copy of the points). */
+int pgpcv_partition_device(pgpcv_ctx *ctx, int64_t n, const double *d_x, const double *d_y,
+                           const double *d_value, const uint8_t *d_role, pgpcv_rect domain,
+                           int32_t kx, int32_t ky, double delta,
+                           pgpcv_partition_info *info_out);
+
+/* Copy the CSR membership of the current partition to caller-allocated host arrays:
+ * train_off int64[N+1], train_idx int32[sum_k], val_off int64[N+1], val_idx int32[sum_m]
+ * (sizes from pgpcv_partition_info).  Any pointer may be NULL to skip it.
+ * Errors: ESTATE (no partition), ECUDA. */
+int pgpcv_partition_export(pgpcv_ctx *ctx, int64_t *train_off, int32_t *train_idx,
+                           int64_t *val_off, int32_t *val_idx);
+
+/* Multi-GPU (Alg.1's parfor over subsets, across the GPUs of one box).
+ * rank in [0, world); world >= 1.  nccl_unique_id: NCCL_UNIQUE_ID_BYTES (128) bytes from
+ * pgpcv_nccl_get_unique_id on rank 0, broadcast by the caller; ignored (may be NULL) when
+ * world == 1.  Creates the NCCL communicator and assigns whole subsets to ranks by LPT on
+ * the cost k_s^3 (ties by subset id), identically on every rank.  Must be called after
+ * pgpcv_partition and before the first pgpcv_cv_loss of that partition (else ESTATE);
+ * without it a ctx owns every subset.  Errors: EINVAL, ESTATE, ENCCL. */
+int pgpcv_shard(pgpcv_ctx *ctx, int rank, int world, const void *nccl_unique_id);
+
+/* Fill `out` (NCCL_UNIQUE_ID_BYTES bytes) with a fresh ncclUniqueId.  Needs no ctx.
+ * Errors: ENCCL (libnccl.so.2 not loadable), EINVAL (NULL). */
+int pgpcv_nccl_get_unique_id(void *out);
+
+/* Alg.1 lines 4-9 for n_params configurations (data resident, parameters streamed;
+ * P:200): for every owned subset with validation data and every config, assemble
+ * Sigma + lambda I from pairwise distances, factor it (FP64 Cholesky), solve, predict the
+ * subset's validation points and sum squared errors; then combine.
+ *   params: host array [n_params].
+ *   loss:   host double[n_params] (required): global C~V per config (SSPE, not RMSPE),
+ *           summed over all subsets (across ranks when world > 1).
+ *   subset_loss: host double[N * n_params] subset-major (entry s*n_params + c), or NULL.
+ *           Subsets without validation data hold exactly 0 (R10).  When world > 1 the
+ *           per-subset array is all-reduced (each entry has one owner), which also makes
+ *           loss[] bit-identical for every world size.
+ *   status: host int32[n_params] or NULL: -1 if config c succeeded, else the smallest
+ *           subset id whose factorization failed (loss[c] = NaN then).
+ * Errors: EINVAL (bad params), ESTATE (no partition), EEMPTY (no validation data at all),
+ * ENUMERIC (some config failed; others valid), ECUDA, ENOMEM, ENCCL. */
+int pgpcv_cv_loss(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, double *loss,
+                  double *subset_loss, int32_t *status);
+
+/* Timing and work counts of the last successful pgpcv_cv_loss on ctx. */
+int pgpcv_last_timing(const pgpcv_ctx *ctx, pgpcv_timing *out);
+
+/* Host-only helper (no GPU needed): LPT assignment of n_items with costs cost[] to
+ * `world` owners -- items in descending cost (ties: ascending index), each to the
+ * currently least-loaded owner (ties: lowest rank).  owner: int32[n_items] out.
+ * This is the rule pgpcv_shard applies to the subsets (cost = k^3 if m > 0 else 0). */
+int pgpcv_lpt_assign(int64_t n_items, const double *cost, int32_t world, int32_t *owner);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGPCV_H */

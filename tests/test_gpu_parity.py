@@ -1,0 +1,268 @@
+"""GPU parity: the CUDA path (through the C ABI, libpgpcv.so) against the CPU oracle on
+the same seeded inputs.
+
+Bar (BASELINE.json north_star): subset membership bit-exact; every per-subset and global
+CV loss within |g - o| <= 1e-9 |o| (FP64); exact zeros where the method gives them
+(R10); bit-exact power-of-two invariants on the GPU itself.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+THREADS = os.cpu_count() or 8
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1912_13132_b200 as pg
+    return pg
+
+
+@pytest.fixture(scope="module")
+def ctx(pg):
+    c = pg.Context(0)
+    yield c
+    c.close()
+
+
+_wl_cache = {}
+
+
+def wl(name, **kw):
+    key = (name, tuple(sorted(kw.items())))
+    if key not in _wl_cache:
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        _wl_cache[key] = workloads.make(name, device=dev, **kw)
+    return _wl_cache[key]
+
+
+def _assert_partition_equal(ctx, w):
+    info = ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    toff, tidx, voff, vidx = ctx.partition_export()
+    ref = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
+    assert np.array_equal(toff, ref.train_off)
+    assert np.array_equal(voff, ref.val_off)
+    assert np.array_equal(tidx, ref.train_idx)
+    assert np.array_equal(vidx, ref.val_idx)
+    assert info["n_train"] == int((w.role == 0).sum()) and info["n_val"] == int((w.role == 1).sum())
+    return ref
+
+
+def _assert_close(g, o, rtol=RTOL):
+    g = np.asarray(g, np.float64)
+    o = np.asarray(o, np.float64)
+    bad = ~(np.abs(g - o) <= rtol * np.abs(o))
+    if bad.any():
+        i = np.argwhere(bad)[:5]
+        raise AssertionError(f"{bad.sum()} entries beyond rtol {rtol}: idx {i.tolist()} "
+                             f"gpu {g[bad][:5]} oracle {o[bad][:5]}")
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_partition_bit_exact(ctx, name):
+    """Alg.1 lines 2-3: GPU counting-sort membership == brute-force oracle."""
+    _assert_partition_equal(ctx, wl(name))
+
+
+def test_cv_loss_c1_full(ctx):
+    w = wl("c1")
+    ref_part = _assert_partition_equal(ctx, w)
+    res = ctx.cv_loss(w.params)
+    ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, w.params, threads=THREADS)
+    _assert_close(res.subset_loss, ref.subset_loss)
+    _assert_close(res.loss, ref.loss)
+    assert res.status.tolist() == [-1]
+
+
+def test_cv_loss_c2_full_grid(ctx):
+    """All 100 subsets x 75 configs of c2 (the paper's 20,000-point size)."""
+    w = wl("c2")
+    ref_part = _assert_partition_equal(ctx, w)
+    res = ctx.cv_loss(w.params)
+    ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, w.params, threads=THREADS)
+    _assert_close(res.subset_loss, ref.subset_loss)
+    _assert_close(res.loss, ref.loss)
+
+
+def test_cv_loss_c3_configs(ctx):
+    """All 1,600 subsets of c3 at the grid corners and the truth."""
+    w = wl("c3")
+    ref_part = _assert_partition_equal(ctx, w)
+    p = w.params[[0, 13, 26]]
+    res = ctx.cv_loss(p)
+    ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, p, threads=THREADS)
+    _assert_close(res.subset_loss, ref.subset_loss)
+    _assert_close(res.loss, ref.loss)
+
+
+def _stratified(k, m, n, seed):
+    rng = np.random.default_rng(seed)
+    N = k.size
+    has = np.nonzero(m > 0)[0]
+    pick = {int(has[np.argmin(k[has])]), int(has[np.argmax(k[has])]), 0, N - 1}
+    pick |= set(rng.choice(has, size=max(0, n - len(pick)), replace=False).tolist())
+    return np.array(sorted(pick))
+
+
+def test_c4_sampled_parity(ctx):
+    """c4 (clustered, uneven k up to ~1,800) at full size: sampled subsets x 2 configs."""
+    w = wl("c4")
+    ref_part = _assert_partition_equal(ctx, w)
+    p = w.params[[0, 63]]
+    res = ctx.cv_loss(p)
+    sub = _stratified(ref_part.k(), ref_part.m(), 48, 4)
+    ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, p, subsets=sub, threads=THREADS)
+    _assert_close(res.subset_loss[sub], ref.subset_loss[sub])
+    # subsets without validation data contribute exactly 0 (R10)
+    empty = np.nonzero(ref_part.m() == 0)[0]
+    assert np.all(res.subset_loss[empty] == 0.0)
+    assert res.loss == pytest.approx(res.subset_loss.sum(axis=0), rel=1e-12)
+
+
+def test_c5_full_size_sampled(ctx):
+    """c5 (5M points, 2,500 subsets, k ~ 4,000) in the bench's launch configuration: all
+    subsets at the truth config; 16 stratified subsets checked one by one on the oracle."""
+    w = wl("c5")
+    ref_part = _assert_partition_equal(ctx, w)
+    truth = np.array([[1.0, 1.0, 0.1]])
+    res = ctx.cv_loss(truth)
+    sub = _stratified(ref_part.k(), ref_part.m(), 16, 5)
+    ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, truth, subsets=sub, threads=THREADS)
+    _assert_close(res.subset_loss[sub], ref.subset_loss[sub])
+    # a nugget-noise floor: RMSPE slightly above sqrt(tau) = 0.316 at the truth
+    rmspe = math.sqrt(res.loss[0] / ref_part.m().sum())
+    assert 0.3 < rmspe < 0.5
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 31, 63, 64, 65, 127, 128, 129, 255, 257, 700])
+def test_ragged_single_subset(ctx, k):
+    """One tile (Eq.7 with N = 1 is Eq.4): k training points not a multiple of the 64-wide
+    block or the 128-row tile, m = 7 validation points."""
+    m = 7
+    rng = np.random.default_rng(1000 + k)
+    n = k + m
+    x, y = rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+    v = rng.standard_normal(n)
+    role = np.zeros(n, np.uint8)
+    role[rng.permutation(n)[:m]] = 1
+    ctx.partition(x, y, v, role, (0, 1, 0, 1), 1, 1, 0.0)
+    p = np.array([[0.1, 1.0, 0.1], [0.5, 2.0, 0.01]])
+    res = ctx.cv_loss(p)
+    ref_part = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
+    ref = oracle.cv_loss(x, y, v, ref_part, p, threads=2)
+    _assert_close(res.subset_loss, ref.subset_loss)
+
+
+def test_empty_and_degenerate_subsets(ctx):
+    """Tiles without validation (loss exactly 0, R10), tiles without training (yhat = 0,
+    loss = sum y_V^2, R11), and an all-test tile."""
+    x = np.array([0.1, 0.2, 0.3, 0.6, 0.7, 0.1, 0.9, 0.8])
+    y = np.array([0.1, 0.2, 0.3, 0.1, 0.2, 0.9, 0.9, 0.6])
+    v = np.array([1.0, -1.0, 0.5, 2.0, -0.5, 1.5, 0.25, 3.0])
+    role = np.array([0, 0, 1, 0, 0, 1, 2, 2], np.uint8)
+    ctx.partition(x, y, v, role, (0, 1, 0, 1), 2, 2, 0.0)
+    res = ctx.cv_loss([[0.3, 1.0, 0.1]])
+    ref_part = oracle.partition(x, y, role, (0, 1, 0, 1), 2, 2, 0.0)
+    ref = oracle.cv_loss(x, y, v, ref_part, [[0.3, 1.0, 0.1]], threads=1)
+    assert res.subset_loss[1, 0] == 0.0 and res.subset_loss[3, 0] == 0.0  # no validation
+    assert res.subset_loss[2, 0] == 1.5 ** 2                                # no training
+    _assert_close(res.subset_loss, ref.subset_loss)
+
+
+def test_non_pd_reports_status(ctx, pg):
+    """Duplicate sites with zero nugget: ENUMERIC, loss NaN, status = first failing subset;
+    the other config is unaffected (R12)."""
+    x = np.array([0.1, 0.1, 0.2, 0.8, 0.9, 0.85])
+    y = np.array([0.1, 0.1, 0.3, 0.8, 0.7, 0.9])
+    v = np.array([1.0, 2.0, 0.5, 0.3, -0.2, 0.4])
+    role = np.array([0, 0, 1, 0, 0, 1], np.uint8)
+    ctx.partition(x, y, v, role, (0, 1, 0, 1), 2, 1, 0.0)
+    res = ctx.cv_loss([[0.2, 1.0, 0.0], [0.2, 1.0, 0.1]])
+    assert res.code == pg.ENUMERIC
+    assert math.isnan(res.loss[0]) and res.status[0] == 0
+    assert res.status[1] == -1
+    ref_part = oracle.partition(x, y, role, (0, 1, 0, 1), 2, 1, 0.0)
+    ref = oracle.cv_loss(x, y, v, ref_part, [[0.2, 1.0, 0.1]], threads=1)
+    _assert_close(res.loss[1:], ref.loss)
+
+
+def test_invariants_bit_exact_on_gpu(ctx):
+    """(2 sigma2, 2 tau) -> identical; y -> 2y -> loss x4 exactly; (x, y, D, delta, theta)
+    x2 -> identical membership and loss (R8; exact power-of-two scaling)."""
+    w = wl("c2")
+    ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    p = w.params[[3, 40]]
+    base = ctx.cv_loss(p).subset_loss
+    p2 = p.copy()
+    p2[:, 1:] *= 2
+    assert np.array_equal(ctx.cv_loss(p2).subset_loss, base)
+    again = ctx.cv_loss(p).subset_loss
+    assert np.array_equal(again, base)  # deterministic
+    one = ctx.cv_loss(p[1:]).subset_loss
+    assert np.array_equal(one[:, 0], base[:, 1])  # batching over configs changes nothing
+    ctx.partition(w.x, w.y, 2 * w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    assert np.array_equal(ctx.cv_loss(p).subset_loss, 4 * base)
+    d2 = tuple(2 * d for d in w.domain)
+    ctx.partition(2 * w.x, 2 * w.y, w.value, w.role, d2, w.kx, w.ky, 2 * w.delta)
+    p3 = p.copy()
+    p3[:, 0] *= 2
+    assert np.array_equal(ctx.cv_loss(p3).subset_loss, base)
+
+
+def test_single_subset_equals_global_and_saturated_shell(ctx):
+    """Eq.7 exactness limits on the GPU: one tile, and a shell wider than D."""
+    x, y, v, role = workloads.random_points(77, 1500, frac_val=0.1)
+    p = [[0.15, 1.0, 0.1]]
+    ctx.partition(x, y, v, role, (0, 1, 0, 1), 1, 1, 0.0)
+    one = ctx.cv_loss(p).loss[0]
+    ctx.partition(x, y, v, role, (0, 1, 0, 1), 3, 3, 1.5)
+    sat = ctx.cv_loss(p).loss[0]
+    assert sat == pytest.approx(one, rel=1e-12)
+    t, w_ = role == 0, role == 1
+    ref = oracle.subset_cv(x[t], y[t], v[t], x[w_], y[w_], v[w_], 0.15, 1.0, 0.1)
+    assert one == pytest.approx(ref, rel=RTOL)
+
+
+def test_partition_rejects_bad_input(ctx, pg):
+    x, y, v, role = workloads.random_points(3, 100)
+    with pytest.raises(pg.PgpcvError) as ei:
+        ctx.partition(x + 1.5, y, v, role, (0, 1, 0, 1), 2, 2, 0.1)
+    assert ei.value.code == pg.EINVAL
+    v2 = v.copy()
+    v2[5] = np.nan
+    with pytest.raises(pg.PgpcvError):
+        ctx.partition(x, y, v2, role, (0, 1, 0, 1), 2, 2, 0.1)
+    ctx.partition(x, y, v, role, (0, 1, 0, 1), 2, 2, 0.1)
+    with pytest.raises(pg.PgpcvError) as ei:
+        ctx.cv_loss([[0.0, 1.0, 0.1]])
+    assert ei.value.code == pg.EINVAL
+    with pytest.raises(pg.PgpcvError) as ei:
+        ctx.partition(x, y, v, np.full(100, 2, np.uint8), (0, 1, 0, 1), 2, 2, 0.1) and None
+        ctx.cv_loss([[0.1, 1.0, 0.1]])
+    assert ei.value.code == pg.EEMPTY
+
+
+def test_partition_device_pointers_match_host(ctx):
+    import torch
+    w = wl("c2")
+    ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    a = ctx.partition_export()
+    la = ctx.cv_loss(w.params[:2]).subset_loss
+    t = [torch.as_tensor(arr).cuda() for arr in (w.x, w.y, w.value, w.role)]
+    ctx.partition_device(*t, w.domain, w.kx, w.ky, w.delta)
+    b = ctx.partition_export()
+    for u, q in zip(a, b):
+        assert np.array_equal(u, q)
+    assert np.array_equal(ctx.cv_loss(w.params[:2]).subset_loss, la)
