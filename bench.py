@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the parallel-CV hot path (BASELINE.json metric: subset CV-loss evals/sec and
+sec per parameter configuration at 5M points; FP64 % of peak).
+
+A "step" is one pass of the whole hot path (Alg.1 lines 4-9) over all
+2,500 subsets of the 5M-point workload c5 for ONE (range, sigma2, nugget) configuration of
+its 125-point grid (steps cycle through the grid): covariance assembly, FP64 Cholesky,
+solves, prediction, loss reduction (and the NCCL all-reduce when N > 1).  The partition
+(Alg.1 lines 2-3, "done once") happens before the timed region for `value`, and
+inside every step for `e2e` (host arrays -> C ABI -> host loss).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5]
+
+N > 1 is launched by torchrun (one rank per GPU); times are CUDA-event times, max over
+ranks.  `--impl reference` times the CPU oracle (the reference arm of this tier) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "subset CV-loss evals/sec (5M pts, one (range, sigma2, nugget) config per step)"
+UNIT = "subset-evals/s"
+
+
+def _env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v not in (None, "") else default
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+        sm, smax, power, reasons = [], [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def _peaks():
+    """FP64 peak (the denominator): P0's measured DMMA number (profiles/r01_p0_fp64_peak.json),
+    with the bf16-derived figure (MEASURED_PEAKS.json x nominal FP64/BF16 ratio) beside it."""
+    p0 = os.path.join(ROOT, "profiles", "r01_p0_fp64_peak.json")
+    meas = None
+    if os.path.exists(p0):
+        meas = json.load(open(p0)).get("dmma_tflops_sustained")
+    derived = None
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        bf16 = json.load(open(mp)).get("bf16_tflops_sustained")
+        if bf16:
+            derived = bf16 * 45.0 / 2250.0  # guide: B200 FP64 tensor 45 TF vs bf16 2.25 PF dense
+    return meas, derived
+
+
+def _traffic():
+    f = os.path.join(ROOT, "profiles", "r01_cv_kernel_dram.json")
+    if os.path.exists(f):
+        try:
+            return json.load(f and open(f)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def _stratified_sample(k, m, count, seed=5):
+    rng = np.random.default_rng(seed)
+    has = np.nonzero(m > 0)[0]
+    order = has[np.argsort(k[has], kind="stable")]
+    pick = set(order[np.linspace(0, order.size - 1, min(count, order.size)).astype(int)].tolist())
+    while len(pick) < min(count, has.size):
+        pick.add(int(rng.choice(has)))
+    return np.array(sorted(pick))
+
+
+def run_reference(args, rank, world):
+    """The reference arm of this tier: the CPU oracle (oracle/) as it stands, timed on the
+    host cores, on the same workload/metric; rank 0 only."""
+    if rank != 0:
+        return 0
+    import oracle
+    import workloads
+
+    dev = "cuda" if _has_cuda() else "cpu"
+    w = workloads.make(args.workload, device=dev)
+    part = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
+    k, m = part.k(), part.m()
+    cores = os.cpu_count() or 1
+    sample = _stratified_sample(k, m, cores)
+    t_total, evals = 0.0, 0
+    for step in range(args.warmup + args.steps):
+        p = w.params[step % len(w.params)][None, :]
+        t0 = time.perf_counter()
+        oracle.cv_loss(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            t_total += dt
+            evals += sample.size
+    value = evals / t_total
+    desc = (f"{sample.size} stratified {args.workload} subsets (k {int(k[sample].min())}-"
+            f"{int(k[sample].max())}) x 1 config per step, oracle.c (-O2, no FMA) as it stands")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config(args, w, part),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _has_cuda():
+    import torch
+    return torch.cuda.is_available()
+
+
+def _config(args, w, part_or_info):
+    if isinstance(part_or_info, dict):
+        N, nv = part_or_info["n_subsets"], part_or_info["n_val"]
+    else:
+        N, nv = part_or_info.n_subsets, int(part_or_info.m().sum())
+    return {"workload": f"{args.workload}: n={w.n:,} on [{w.domain[0]:g},{w.domain[1]:g}]^2, "
+                        f"{w.kx}x{w.ky} tiles, delta={w.delta:g}, {len(w.params)}-config grid "
+                        f"(one config per step), FP64",
+            "n_points": w.n, "n_subsets": N, "n_val": nv, "grid_configs": len(w.params),
+            "configs_per_step": 1, "parallelism": f"subsets sharded by LPT over {args.gpus} GPU(s)",
+            "l2": "no flush: per-step factor working set (148 slots x up to 142 MB) >> 126 MB L2"}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_1912_13132_b200 as pg
+    import workloads
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    w = workloads.make(args.workload, device="cuda")
+    C = len(w.params)
+    # inputs resident in HBM (value) and pinned host copies (e2e)
+    dx = torch.as_tensor(w.x, device="cuda")
+    dy = torch.as_tensor(w.y, device="cuda")
+    dv = torch.as_tensor(w.value, device="cuda")
+    dr = torch.as_tensor(w.role, device="cuda")
+    hx, hy, hv, hr = (torch.as_tensor(a).pin_memory().numpy() for a in (w.x, w.y, w.value, w.role))
+
+    ctx = pg.Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    info = ctx.partition_device(dx, dy, dv, dr, w.domain, w.kx, w.ky, w.delta)
+    uid = None
+    if world > 1:
+        obj = [pg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx.shard(rank, world, uid)
+    toff, _, voff, _ = ctx.partition_export()
+    kk, mm = np.diff(toff), np.diff(voff)
+    evals_per_step = int((mm > 0).sum())  # all subsets with validation data, over all ranks
+
+    def step(i):
+        return ctx.cv_loss(w.params[i % C][None, :], want_subset_loss=False)
+
+    for i in range(args.warmup):
+        step(i)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    barrier()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern_ms, kern_flops, launches, losses = 0.0, 0.0, 0, []
+    e0.record(stream)
+    for i in range(args.steps):
+        r = step(args.warmup + i)
+        t = ctx.last_timing()
+        kern_ms += t["kernel_ms"]
+        kern_flops += t["flops"]
+        launches += t["launches"]
+        losses.append(float(r.loss[0]))
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    t_ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+
+    # e2e: host arrays through the public API every step (H2D of the points, partition,
+    # cv_loss, D2H of the loss); timed with events around synchronous calls.
+    barrier()
+    ctx.set_stream(stream.cuda_stream)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for i in range(args.steps):
+        ctx.partition(hx, hy, hv, hr, w.domain, w.kx, w.ky, w.delta)
+        ctx.cv_loss(w.params[(args.warmup + i) % C][None, :], want_subset_loss=False)
+    f1.record(stream)
+    barrier()
+    e2e_ms = f0.elapsed_time(f1)
+    if dist:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    # dominant kernel roofline (FP64 tensor path), this rank's launches
+    achieved = kern_flops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else 0.0
+    peak, derived = _peaks()
+    value = evals_per_step * args.steps / (t_ms * 1e-3)
+    n = w.n
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(args, w, info),
+        "sec_per_config": t_ms / args.steps / 1e3,
+        "fp64_pct_of_peak": 100.0 * achieved / peak if peak else None,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": _traffic(),
+                     "kernel": "cv_kernel (assembly + DMMA Cholesky + solves + prediction + SSPE)",
+                     "kernel_ms_per_launch": kern_ms / args.steps,
+                     "flops_per_launch": kern_flops / args.steps,
+                     "peak_source": "measured FP64 DMMA, probes/p0_fp64_peak (profiles/r01_p0_fp64_peak.json)",
+                     "peak_bf16_derived": derived},
+        "e2e": {"value": evals_per_step * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": int(n * (8 * 3 + 1) + 24), "d2h_bytes_per_step": 8 + 4},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "subset_k": {"min": int(kk[mm > 0].min()), "median": float(np.median(kk[mm > 0])),
+                     "max": int(kk.max())},
+        "loss_first_step": losses[0],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = _cpu_baseline(w, toff, voff, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def _cpu_baseline(w, toff, voff, args):
+    """The oracle as it stands on the host cores: a bounded sample of the same workload
+    (one c5 subset per core x 1 config, ~15 s), scaled to evals/s."""
+    import oracle
+
+    part = oracle.Partition(toff, None, voff, None, w.kx, w.ky)
+    # membership lists from the oracle's own brute-force partition (independent of the GPU)
+    part = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
+    cores = os.cpu_count() or 1
+    sample = _stratified_sample(part.k(), part.m(), cores)
+    p = w.params[args.warmup % len(w.params)][None, :]
+    t0 = time.perf_counter()
+    oracle.cv_loss(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": sample.size / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{sample.size} stratified {args.workload} subsets x 1 config "
+                      f"(k {int(part.k()[sample].min())}-{int(part.k()[sample].max())}), "
+                      f"{dt:.1f} s on {cores} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
