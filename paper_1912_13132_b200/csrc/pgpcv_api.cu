@@ -198,7 +198,7 @@ void assign_owned(pgpcv_ctx *ctx) {
     for (int64_t s = 0; s < ctx->N; ++s) {
         const double k = (double)(ctx->h_train_off[s + 1] - ctx->h_train_off[s]);
         const double m = (double)(ctx->h_val_off[s + 1] - ctx->h_val_off[s]);
-        cost[s] = m > 0 ? k * k * k + 1.0 : 0.0;  // +1: k = 0 subsets still cost a launch slot
+        cost[s] = m > 0 ? k * k * k : 0.0;  // the rule documented in pgpcv.h
     }
     std::vector<int32_t> owner(ctx->N);
     pgpcv_lpt_assign(ctx->N, cost.data(), ctx->world, owner.data());
