@@ -1,8 +1,8 @@
 // cv_kernel.cu -- the hot path of parallel cross-validation on B200 (sm_100a), FP64.
 //
-// One persistent CTA per factorization slot pulls (subset s, config c) work items in LPT
-// order and, for each, evaluates the subset's local SSPE z_i of Alg.1 line 7 (PAPER.md
-// P:224) exactly as Eq.3/Eq.4 define it:
+// Persistent CTAs (two per SM) pull (subset s, config c) work items in LPT order and, for
+// each, evaluate the subset's local SSPE z_i of Alg.1 line 7 exactly as
+// Eq.3/Eq.4 define it:
 //
 //   A  = Sigma(theta) + lambda I,  Sigma_ij = exp(-||t_i - t_j|| / theta)
 //   A  = L L^T                      blocked left-looking Cholesky (FP64)
@@ -20,15 +20,19 @@
 // Left-looking step for block column j (width NB = 64, columns j0..j0+jw-1), for every
 // row tile of MT = 128 rows r0.. (rows j0..k):
 //   acc    = L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T       -- FP64 DMMA (mma.m8n8k4),
-//            operands streamed HBM/L2 -> SMEM by a 3-stage cp.async pipeline, KC = 32
-//   C      = A[r0:r0+MT, j0:j0+NB] - acc                    -- generated on the fly
+//            operands streamed HBM/L2 -> SMEM by a 3-stage cp.async pipeline (KC = 16)
+//   C      = A[r0:r0+MT, j0:j0+NB] - acc                    -- generated in registers
 //   tile 0 : L_jj = chol(C[0:jw, 0:jw]) and Linv = L_jj^{-1}, fused, in SMEM
-//   X      = C . Linv^T                                      -- FP64 DMMA (TRSM as GEMM)
+//   X      = C . Linv^T                                      -- FP64 DMMA; the A operand
+//            comes straight from the accumulator registers via warp shuffles
 //   L[r0:, j0:j0+jw] = X   (tile 0: its first jw rows are L_jj itself)
 //
-// SMEM operand tiles are k-major with a row stride of MT+4 / NB+4 doubles: a stride of
-// 8 (mod 32) 4-byte words makes the DMMA A/B fragment loads (lane (g,t) reads element
-// [t][g]) conflict-free per half-warp.
+// Each warp owns 16 full rows of a tile (8 warps x 16 = 128), so the TRSM needs no
+// cross-warp exchange.  SMEM operand tiles are k-major with a row stride of MT+4 / NB+4
+// doubles: a stride of 8 (mod 32) 4-byte words makes the DMMA fragment loads (lane (g,t)
+// reads element [t][g]) conflict-free per half-warp.  113.7 KB of SMEM and <= 128
+// registers per thread let two CTAs share an SM, so one CTA's barriers, epilogue,
+// diagonal factorization and back-substitution overlap the other's DMMA stream.
 #include <cmath>
 #include <cstdint>
 
@@ -40,24 +44,24 @@ namespace {
 constexpr int MT = kMT;
 constexpr int NB = kNB;
 constexpr int NT = kThreads;
-constexpr int KC = 32;
+constexpr int NWARP = NT / 32;
+constexpr int KC = 16;
 constexpr int STAGES = 3;
 constexpr int AS = MT + 4;  // 132 doubles = 264 words == 8 (mod 32)
 constexpr int BS = NB + 4;  // 68 doubles  = 136 words == 8 (mod 32)
-constexpr int LJS = NB + 1; // 65: odd stride for the back-substitution diagonal block
+constexpr int LJS = NB + 1; // 65: row stride of the diagonal block in SMEM
 constexpr int A_STAGE = KC * AS;
 constexpr int B_STAGE = KC * BS;
-constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE); // 19,200 doubles
-constexpr int CS_DBL = NB * AS;                         // C tile, aliases the stages
-constexpr int BT_DBL = NB * BS;                         // Linv^T tile
-constexpr int COORD_DBL = 2 * MT + 3 * NB;
-constexpr int MISC_DBL = NB + 16;
-constexpr size_t SMEM_BYTES = sizeof(double) * (STAGE_DBL + BT_DBL + COORD_DBL + MISC_DBL);
-static_assert(CS_DBL <= STAGE_DBL, "C tile must fit in the stage buffers");
+constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE);  // 9,600 doubles
+constexpr int BT_DBL = NB * BS;                          // Linv^T tile
+constexpr int COL_DBL = 3 * NB;                          // block-column x, y, value
+constexpr int MISC_DBL = NB + NWARP;                     // sqrt pivots, warp partials
+constexpr size_t SMEM_BYTES = sizeof(double) * (STAGE_DBL + BT_DBL + COL_DBL + MISC_DBL);
+static_assert(NB * LJS <= STAGE_DBL, "diagonal block must fit in the stage buffers");
 static_assert(NB * LJS <= BT_DBL, "back-substitution block must fit in the Linv buffer");
-static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+static_assert(SMEM_BYTES <= 115712, "two CTAs per SM");
 static_assert((AS * 2) % 32 == 8 && (BS * 2) % 32 == 8, "fragment-load strides");
-static_assert(MT == 4 * 32 && NB == 2 * 32 && NT == 256, "8 warps as 4 (M) x 2 (N), 32x32 each");
+static_assert(MT == 16 * NWARP && NB == 64, "each warp owns 16 rows x 64 columns");
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -84,62 +88,45 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Stage KC columns (kk..kk+KC-1) of two row ranges of L into SMEM, k-major:
-//   As[q][rr] = L[r0 + rr, kk + q]  (rows >= nva zero-filled)
-//   Bs[q][rr] = L[j0 + rr, kk + q]  (rows >= nvb zero-filled)
-__device__ __forceinline__ void load_stage(double *As, double *Bs, const double *L, int64_t ld,
-                                           int r0, int nva, int j0, int nvb, int kk, int tid) {
-#pragma unroll
-    for (int i = 0; i < (KC * MT / 2) / NT; ++i) {
-        const int e = tid + i * NT;
-        const int q = e / (MT / 2);
-        const int rr = (e % (MT / 2)) * 2;
-        const int row = r0 + rr;
-        const int nbytes = row + 2 <= nva ? 16 : (row < nva ? 8 : 0);
-        const double *src = nbytes ? L + (size_t)(kk + q) * ld + row : L;
-        cp_async16(As + q * AS + rr, src, nbytes);
-    }
-#pragma unroll
-    for (int i = 0; i < (KC * NB / 2) / NT; ++i) {
-        const int e = tid + i * NT;
-        const int q = e / (NB / 2);
-        const int rr = (e % (NB / 2)) * 2;
-        const int row = j0 + rr;
-        const int nbytes = row + 2 <= nvb ? 16 : (row < nvb ? 8 : 0);
-        const double *src = nbytes ? L + (size_t)(kk + q) * ld + row : L;
-        cp_async16(Bs + q * BS + rr, src, nbytes);
-    }
-}
+struct TileLoader {
+    // A: 4 x 16-byte chunks per thread per stage (columns q0a + 4i, rows rra..rra+1)
+    // B: 2 x 16-byte chunks per thread per stage (columns q0b + 8i, rows rrb..rrb+1)
+    const double *ga;
+    const double *gb;
+    int64_t ld;
+    int sa, sb;      // SMEM offsets (doubles) inside a stage
+    int na, nb;      // bytes to copy (16, 8 or 0: zero-fill past the last valid row)
 
-// acc[i][j] += A[wm*32 + 8i .., k] * B[k, wn*32 + 8j ..] over ksteps*4 values of k, with
-// A stored k-major at stride as and B stored k-major at stride bs.
-template <int KSTEPS>
-__device__ __forceinline__ void mma_tile(double (&acc)[4][4][2], const double *As, int as,
-                                         const double *Bs, int bs, int wm, int wn, int g, int t) {
-#pragma unroll
-    for (int k4 = 0; k4 < KSTEPS; ++k4) {
-        const double *ap = As + (k4 * 4 + t) * as + wm * 32 + g;
-        const double *bp = Bs + (k4 * 4 + t) * bs + wn * 32 + g;
-        double a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = ap[i * 8];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = bp[j * 8];
+    __device__ __forceinline__ void init(const double *L, int64_t ld_, int r0, int nva, int j0,
+                                         int nvb, int tid) {
+        ld = ld_;
+        const int q0a = tid >> 6, rra = (tid & 63) * 2;
+        const int q0b = tid >> 5, rrb = (tid & 31) * 2;
+        const int ra = r0 + rra, rb = j0 + rrb;
+        na = ra + 2 <= nva ? 16 : (ra < nva ? 8 : 0);
+        nb = rb + 2 <= nvb ? 16 : (rb < nvb ? 8 : 0);
+        ga = na ? L + (size_t)q0a * ld + ra : L;
+        gb = nb ? L + (size_t)q0b * ld + rb : L;
+        sa = q0a * AS + rra;
+        sb = A_STAGE + q0b * BS + rrb;
+    }
+    __device__ __forceinline__ void load(double *stage, int kk) const {
+        const size_t off = (size_t)kk * ld;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
+            cp_async16(stage + sa + i * 4 * AS, na ? ga + off + (size_t)(4 * i) * ld : ga, na);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+        for (int i = 0; i < 2; ++i)
+            cp_async16(stage + sb + i * 8 * BS, nb ? gb + off + (size_t)(8 * i) * ld : gb, nb);
     }
-}
+};
 
-__global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
+__global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     extern __shared__ __align__(16) double smem[];
     double *stage = smem;
-    double *Cs = smem;                  // aliases the stages after the update GEMM
+    double *LJ = smem;                  // diagonal block [r][c], aliases the stages
     double *Bt = smem + STAGE_DBL;      // Bt[q*BS + n] = Linv[n][q]
-    double *rx = Bt + BT_DBL;           // row-tile coordinates
-    double *ry = rx + MT;
-    double *cx = ry + MT;               // block-column coordinates and values
+    double *cx = Bt + BT_DBL;           // block-column coordinates and values
     double *cy = cx + NB;
     double *cv = cy + NB;
     double *dg = cv + NB;               // sqrt pivots of the diagonal block
@@ -150,7 +137,6 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = warp & 3, wn = warp >> 2;
     double *L = a.work + (size_t)blockIdx.x * a.slot_stride;
 
     for (;;) {
@@ -189,76 +175,103 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
             }
             for (int rt = 0; rt < ntiles; ++rt) {
                 const int r0 = j0 + rt * MT;
-                for (int i = tid; i < MT; i += NT) {
-                    const int r = r0 + i;
-                    rx[i] = r < k ? __ldg(tx + r) : 0.0;
-                    ry[i] = r < k ? __ldg(ty + r) : 0.0;
-                }
-                double acc[4][4][2];
+                const int rbase = r0 + warp * 16;  // this warp's first row
+                double acc[2][8][2];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+                    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
                 // acc = L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
                 const int nk = j0 / KC;
                 if (nk > 0) {
+                    TileLoader ldr;
+                    ldr.init(L, ld, r0, k + 1, j0, k, tid);
 #pragma unroll
                     for (int st = 0; st < STAGES - 1; ++st) {
-                        if (st < nk)
-                            load_stage(stage + st * (A_STAGE + B_STAGE),
-                                       stage + st * (A_STAGE + B_STAGE) + A_STAGE, L, ld, r0,
-                                       k + 1, j0, k, st * KC, tid);
+                        if (st < nk) ldr.load(stage + st * (A_STAGE + B_STAGE), st * KC);
                         cp_async_commit();
                     }
                     for (int kc = 0; kc < nk; ++kc) {
                         cp_async_wait<STAGES - 2>();
                         __syncthreads();
                         const int nxt = kc + STAGES - 1;
-                        if (nxt < nk) {
-                            double *sb = stage + (nxt % STAGES) * (A_STAGE + B_STAGE);
-                            load_stage(sb, sb + A_STAGE, L, ld, r0, k + 1, j0, k, nxt * KC, tid);
-                        }
+                        if (nxt < nk) ldr.load(stage + (nxt % STAGES) * (A_STAGE + B_STAGE), nxt * KC);
                         cp_async_commit();
                         const double *As = stage + (kc % STAGES) * (A_STAGE + B_STAGE);
-                        mma_tile<KC / 4>(acc, As, AS, As + A_STAGE, BS, wm, wn, g, t);
+                        const double *Bs = As + A_STAGE;
+#pragma unroll
+                        for (int k4 = 0; k4 < KC / 4; ++k4) {
+                            const double *ap = As + (k4 * 4 + t) * AS + warp * 16 + g;
+                            const double *bp = Bs + (k4 * 4 + t) * BS + g;
+                            double af[2], bf[8];
+                            af[0] = ap[0];
+                            af[1] = ap[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                                for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
+                        }
                     }
                     cp_async_wait<0>();
                 }
-                __syncthreads();
+                __syncthreads();  // stages free (LJ may alias them); cx/cy/cv visible
 
-                // C = A - acc, A generated on the fly (Eq.3 second line)
+                // C = A - acc, A generated on the fly (Eq.3 second line), in registers
+                {
+                    double rx[2], ry[2];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < 2; ++i) {
+                        const int r = rbase + i * 8 + g;
+                        rx[i] = r < k ? __ldg(tx + r) : 0.0;
+                        ry[i] = r < k ? __ldg(ty + r) : 0.0;
+                    }
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int i = 0; i < 2; ++i)
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int ml = wm * 32 + i * 8 + g;
-                            const int nl = wn * 32 + j * 8 + 2 * t + e;
-                            const int r = r0 + ml, cc = j0 + nl;
-                            double av;
-                            if (cc >= k || r > k) av = 0.0;
-                            else if (r == k) av = cv[nl];           // bordered row: y_T
-                            else if (r == cc) av = 1.0 + lam;       // exp(0) + lambda
-                            else if (r < cc) av = 0.0;              // upper triangle: unused
-                            else {
-                                const double dx = rx[ml] - cx[nl], dy = ry[ml] - cy[nl];
-                                av = exp(sqrt(dx * dx + dy * dy) * ninv);
+                        for (int j = 0; j < 8; ++j)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int r = rbase + i * 8 + g;
+                                const int nl = j * 8 + 2 * t + e;
+                                const int cc = j0 + nl;
+                                double av;
+                                if (cc >= k || r > k) av = 0.0;
+                                else if (r == k) av = cv[nl];        // bordered row: y_T
+                                else if (r == cc) av = 1.0 + lam;    // exp(0) + lambda
+                                else if (r < cc) av = 0.0;           // upper triangle: unused
+                                else {
+                                    const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
+                                    av = exp(sqrt(dx * dx + dy * dy) * ninv);
+                                }
+                                acc[i][j][e] = av - acc[i][j][e];
                             }
-                            Cs[nl * AS + ml] = av - acc[i][j][e];
-                        }
-                __syncthreads();
+                }
 
                 if (rt == 0) {
-                    // Fused unblocked Cholesky of C[0:jw,0:jw] and inverse of its factor.
+                    // Diagonal block to SMEM, then fused unblocked Cholesky + inverse.
+                    if (warp < NB / 16) {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int rl = warp * 16 + i * 8 + g;
+                                    const int nl = j * 8 + 2 * t + e;
+                                    if (nl <= rl) LJ[rl * LJS + nl] = acc[i][j][e];
+                                }
+                    }
                     for (int e = tid; e < BT_DBL; e += NT) Bt[e] = 0.0;
                     if (tid == 0) s_fail = 0;
                     __syncthreads();
-                    for (int i = tid; i < jw; i += NT) Bt[i * BS + i] = 1.0;
+                    if (tid < NB) Bt[tid * BS + tid] = 1.0;
                     __syncthreads();
+                    const int r = tid & (NB - 1), cg = tid >> 6;  // row, column group (0..3)
                     for (int q = 0; q < jw; ++q) {
-                        const double d = Cs[q * AS + q];
+                        const double d = LJ[q * LJS + q];
                         if (!(d > 0.0)) {  // not positive definite (R12); uniform decision
                             if (tid == 0) s_fail = 1;
                             break;
@@ -266,17 +279,14 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
                         const double sd = sqrt(d);
                         const double inv = 1.0 / sd;
                         if (tid == 0) dg[q] = sd;
-                        for (int r = q + 1 + tid; r < jw; r += NT) Cs[q * AS + r] *= inv;
-                        for (int i = tid; i <= q; i += NT) Bt[i * BS + q] *= inv;
+                        if (cg == 0 && r > q && r < jw) LJ[r * LJS + q] *= inv;
+                        if (cg == 1 && r <= q) Bt[r * BS + q] *= inv;
                         __syncthreads();
-                        const int w = jw - q - 1;
-                        for (int e = tid; e < w * w; e += NT) {
-                            const int cc = q + 1 + e / w, r = q + 1 + e % w;
-                            if (r >= cc) Cs[cc * AS + r] -= Cs[q * AS + r] * Cs[q * AS + cc];
-                        }
-                        for (int e = tid; e < w * (q + 1); e += NT) {
-                            const int n = q + 1 + e % w, i = e / w;
-                            Bt[i * BS + n] -= Cs[q * AS + n] * Bt[i * BS + q];
+                        if (r > q && r < jw) {
+                            const double lrq = LJ[r * LJS + q];
+                            for (int cc = q + 1 + cg; cc <= r; cc += 4)
+                                LJ[r * LJS + cc] -= lrq * LJ[cc * LJS + q];
+                            for (int i = cg; i <= q; i += 4) Bt[i * BS + r] -= lrq * Bt[i * BS + q];
                         }
                         __syncthreads();
                     }
@@ -285,35 +295,72 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
                         failed = true;
                         break;
                     }
+                    // L_jj -> the factor (lower triangle; the diagonal from the pivots)
+                    for (int e = tid; e < jw * jw; e += NT) {
+                        const int cc = e / jw, rr = e % jw;
+                        if (rr >= cc)
+                            L[(size_t)(j0 + cc) * ld + j0 + rr] = rr == cc ? dg[cc] : LJ[rr * LJS + cc];
+                    }
                 }
 
-                // X = C . Linv^T (triangular solve against L_jj^T as a GEMM)
+                // X = C . Linv^T (triangular solve against L_jj^T as a GEMM).  The A
+                // fragment for k-slice sl (columns 4sl..4sl+3) of row block i is
+                // C[g][4sl + t], held by lane 4g + 2(sl&1) + t/2 as element t&1 of
+                // acc[i][sl/2].  (Rows of the diagonal block itself are discarded: L_jj
+                // was stored above.)
+                // Two passes of 32 output columns keep C (64 registers) plus one half of X
+                // (32 registers) live, within the 128-register budget of 2 CTAs per SM.
+                const int rskip = rt == 0 ? j0 + jw : 0;  // first row below L_jj
+                const int src_lo = (g << 2) + (t >> 1);
+                const bool odd = t & 1;
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int h = 0; h < 2; ++h) {
+                    double xo[2][4][2];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-                mma_tile<NB / 4>(acc, Cs, AS, Bt, BS, wm, wn, g, t);
-
+                    for (int i = 0; i < 2; ++i)
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                        for (int j = 0; j < 4; ++j) xo[i][j][0] = xo[i][j][1] = 0.0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int sl = 0; sl < NB / 4; ++sl) {
+                        const int src = src_lo + 2 * (sl & 1);
+                        double af[2];
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int ml = wm * 32 + i * 8 + g;
-                            const int nl = wn * 32 + j * 8 + 2 * t + e;
-                            const int r = r0 + ml;
-                            if (nl >= jw || r > k) continue;
-                            double val;
-                            if (rt == 0 && ml < jw) {
-                                if (ml < nl) continue;
-                                val = ml == nl ? dg[nl] : Cs[nl * AS + ml];
-                            } else {
-                                val = acc[i][j][e];
-                            }
-                            L[(size_t)(j0 + nl) * ld + r] = val;
+                        for (int i = 0; i < 2; ++i) {
+                            const double v0 = __shfl_sync(0xffffffffu, acc[i][sl >> 1][0], src);
+                            const double v1 = __shfl_sync(0xffffffffu, acc[i][sl >> 1][1], src);
+                            af[i] = odd ? v1 : v0;
                         }
-                __threadfence_block();
+                        const double *bp = Bt + (sl * 4 + t) * BS + h * 32 + g;
+                        double bf[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) bf[j] = bp[j * 8];
+                        // Linv^T is upper triangular: B[q][n] = 0 for q > n, so k-slice
+                        // sl contributes to column block jj only if 4 sl <= 8 jj + 7.
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+#pragma unroll
+                            for (int i = 0; i < 2; ++i)
+                                if (sl <= 2 * (h * 4 + j) + 1) dmma(xo[i][j], af[i], bf[j]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int r = rbase + i * 8 + g;
+                                const int nl = h * 32 + j * 8 + 2 * t + e;
+                                if (nl < jw && r <= k && r >= rskip)
+                                    L[(size_t)(j0 + nl) * ld + r] = xo[i][j][e];
+                            }
+                }
+                if (rt == ntiles - 1) {
+                    // The factor columns just written are re-read through L2 only
+                    // (cp.async.cg, ld.global.cg) by other threads of this CTA in later
+                    // block columns and in the back-substitution: make them visible at GPU
+                    // scope (L2) before the barrier, not just at CTA scope (L1).
+                    __threadfence();
+                }
                 __syncthreads();
             }
         }
@@ -327,14 +374,14 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
         }
 
         // ---------------- backward substitution L^T alpha = z ----------------
-        double *alpha = stage;  // k doubles (k <= STAGE_DBL)
-        double *LJ = Bt;        // NB x LJS
-        double *tvec = rx;      // NB
+        double *alpha = k <= STAGE_DBL ? stage : L + (size_t)ld * k;  // SMEM when it fits
+        double *LB = Bt;        // diagonal block, [row][col] stride LJS
+        double *tvec = cx;      // NB
         for (int jb = nblk - 1; jb >= 0; --jb) {
             const int j0 = jb * NB;
             const int jw = min(NB, k - j0);
             const int rs = j0 + jw;
-            for (int cl = warp; cl < jw; cl += NT / 32) {
+            for (int cl = warp; cl < jw; cl += NWARP) {
                 const double *col = L + (size_t)(j0 + cl) * ld;
                 double sum = 0.0;
                 for (int r = rs + lane; r < k; r += 32) sum += __ldcg(col + r) * alpha[r];
@@ -343,7 +390,7 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
             }
             for (int e = tid; e < jw * jw; e += NT) {
                 const int cc = e / jw, rr = e % jw;  // column cc, row rr of the block
-                if (rr >= cc) LJ[rr * LJS + cc] = __ldcg(L + (size_t)(j0 + cc) * ld + j0 + rr);
+                if (rr >= cc) LB[rr * LJS + cc] = __ldcg(L + (size_t)(j0 + cc) * ld + j0 + rr);
             }
             __syncthreads();
             if (warp == 0) {
@@ -351,9 +398,9 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
                 double t1 = lane + 32 < jw ? tvec[lane + 32] : 0.0;
                 for (int cc = jw - 1; cc >= 0; --cc) {
                     const double tc = __shfl_sync(0xffffffffu, cc < 32 ? t0 : t1, cc & 31);
-                    const double al = tc / LJ[cc * LJS + cc];
-                    if (lane < cc) t0 -= LJ[cc * LJS + lane] * al;
-                    if (lane + 32 < cc) t1 -= LJ[cc * LJS + lane + 32] * al;
+                    const double al = tc / LB[cc * LJS + cc];
+                    if (lane < cc) t0 -= LB[cc * LJS + lane] * al;
+                    if (lane + 32 < cc) t1 -= LB[cc * LJS + lane + 32] * al;
                     if (lane == 0) alpha[j0 + cc] = al;
                 }
             }
@@ -363,7 +410,7 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
         // ---------------- prediction and squared error (Eq.3, Eq.4) ----------------
         const double *vx = a.vx + voff, *vy = a.vy + voff, *vv = a.vv + voff;
         double part = 0.0;
-        for (int v = warp; v < m; v += NT / 32) {
+        for (int v = warp; v < m; v += NWARP) {
             const double px = __ldg(vx + v), py = __ldg(vy + v);
             double sum = 0.0;
             for (int j = lane; j < k; j += 32) {
@@ -378,7 +425,7 @@ __global__ void __launch_bounds__(NT, 1) cv_kernel(CvArgs a) {
         __syncthreads();
         if (tid == 0) {
             double l = 0.0;
-            for (int w = 0; w < NT / 32; ++w) l += red[w];
+            for (int w = 0; w < NWARP; ++w) l += red[w];
             a.subset_loss[(int64_t)s * a.C + c] = l;
             a.fail[(int64_t)s * a.C + c] = 0;
         }
@@ -407,7 +454,13 @@ __global__ void reduce_kernel(const double *subset_loss, const uint8_t *fail, in
 }  // namespace
 
 size_t cv_kernel_smem_bytes() { return SMEM_BYTES; }
-int cv_kernel_max_k() { return STAGE_DBL; }
+int cv_kernel_max_k() { return 1 << 20; }  // bounded by the factor workspace, not SMEM
+size_t cv_kernel_slot_doubles(int64_t kmax) {
+    // factor (ld x k) + alpha when it does not fit in SMEM
+    // (rounded to 256 B: every slot base must keep the 16-B alignment cp.async needs)
+    const size_t d = (size_t)factor_ld(kmax) * (size_t)(kmax > 0 ? kmax : 1) + (size_t)kmax;
+    return (d + 31) / 32 * 32;
+}
 
 cudaError_t cv_kernel_occupancy(int *blocks_per_sm) {
     cudaError_t e = cudaFuncSetAttribute(cv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

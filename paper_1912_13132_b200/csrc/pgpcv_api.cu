@@ -555,7 +555,11 @@ int pgpcv_cv_loss(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, d
 
     // factor workspace: one column-major (k+1) x k factor per resident CTA
     int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_items, 1));
-    const size_t slot_stride = (size_t)factor_ld(kmax) * (size_t)std::max<int64_t>(kmax, 1);
+    if (const char *env = getenv("PGPCV_MAX_SLOTS")) {  // diagnostics: cap resident CTAs
+        const int cap = atoi(env);
+        if (cap > 0) slots = std::min(slots, cap);
+    }
+    const size_t slot_stride = cv_kernel_slot_doubles(kmax);
     while (true) {
         cudaError_t e = ctx->work.ensure((size_t)slots * slot_stride);
         if (e == cudaSuccess) break;

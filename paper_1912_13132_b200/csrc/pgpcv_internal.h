@@ -33,6 +33,7 @@ constexpr int kNB = 64;         // block-column width of the left-looking Choles
 constexpr int kThreads = 256;   // 8 warps
 size_t cv_kernel_smem_bytes();
 int cv_kernel_max_k();
+size_t cv_kernel_slot_doubles(int64_t kmax);  // factor + back-substitution scratch
 // leading dimension (doubles) of a k-point factor: column-major (k+1) x k, +1 bordered row
 __host__ __device__ inline int64_t factor_ld(int64_t k) { return ((k + 1 + 15) / 16) * 16; }
 
