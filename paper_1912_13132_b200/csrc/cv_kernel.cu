@@ -19,9 +19,13 @@
 //
 // Left-looking step for block column j (width NB = 64, columns j0..j0+jw-1), for every
 // row tile of MT = 128 rows r0.. (rows j0..k):
-//   acc    = L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T       -- FP64 DMMA (mma.m8n8k4),
-//            operands streamed HBM/L2 -> SMEM by a 3-stage cp.async pipeline (KC = 16)
-//   C      = A[r0:r0+MT, j0:j0+NB] - acc                    -- generated in registers
+//   acc    = -A[r0:r0+MT, j0:j0+NB]                         -- generated in registers while
+//            the tile's first operand chunks are in flight
+//   acc   += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T       -- FP64 DMMA (mma.m8n8k4),
+//            operands streamed HBM/L2 -> SMEM by 1-D bulk copies (cp.async.bulk, one
+//            column of the tile per copy) issued by warp 0, 3 stages of KC = 16 columns
+//            tracked by full/empty mbarriers (no CTA-wide barrier in the loop)
+//   C      = -acc
 //   tile 0 : L_jj = chol(C[0:jw, 0:jw]) and Linv = L_jj^{-1}, fused, in SMEM
 //   X      = C . Linv^T                                      -- FP64 DMMA; the A operand
 //            comes straight from the accumulator registers via warp shuffles
@@ -63,15 +67,41 @@ static_assert(SMEM_BYTES <= 115712, "two CTAs per SM");
 static_assert((AS * 2) % 32 == 8 && (BS * 2) % 32 == 8, "fragment-load strides");
 static_assert(MT == 16 * NWARP && NB == 64, "each warp owns 16 rows x 64 columns");
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
-                 "r"(src_bytes));
+// ---------------------------------------------------------------- mbarrier / bulk copy
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// 1-D bulk copy global -> shared (async proxy), completion counted on `bar` in bytes.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.global;\n fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // D = A(8x4, row) * B(4x8, col) + D on the FP64 tensor path (SASS DMMA.8x8x4).
@@ -88,41 +118,33 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-struct TileLoader {
-    // A: 4 x 16-byte chunks per thread per stage (columns q0a + 4i, rows rra..rra+1)
-    // B: 2 x 16-byte chunks per thread per stage (columns q0b + 8i, rows rrb..rrb+1)
-    const double *ga;
-    const double *gb;
-    int64_t ld;
-    int sa, sb;      // SMEM offsets (doubles) inside a stage
-    int na, nb;      // bytes to copy (16, 8 or 0: zero-fill past the last valid row)
+constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));  // 24,576 B
 
-    __device__ __forceinline__ void init(const double *L, int64_t ld_, int r0, int nva, int j0,
-                                         int nvb, int tid) {
-        ld = ld_;
-        const int q0a = tid >> 6, rra = (tid & 63) * 2;
-        const int q0b = tid >> 5, rrb = (tid & 31) * 2;
-        const int ra = r0 + rra, rb = j0 + rrb;
-        na = ra + 2 <= nva ? 16 : (ra < nva ? 8 : 0);
-        nb = rb + 2 <= nvb ? 16 : (rb < nvb ? 8 : 0);
-        ga = na ? L + (size_t)q0a * ld + ra : L;
-        gb = nb ? L + (size_t)q0b * ld + rb : L;
-        sa = q0a * AS + rra;
-        sb = A_STAGE + q0b * BS + rrb;
+// Operand chunk n of the running sequence (stage n % STAGES, use n / STAGES): warp 0
+// waits until every warp released the stage's previous use, then its 32 lanes each
+// issue one bulk copy -- lanes 0..15 the A columns (MT doubles), 16..31 the B columns
+// (NB doubles) -- for columns kk..kk+KC-1 of the factor.  Rows past the matrix are
+// copied as whatever the workspace holds; they only reach discarded outputs (see the
+// masking of acc after the update).
+__device__ __forceinline__ void issue_chunk(uint32_t n, double *stage, uint64_t *full, uint64_t *empty,
+                                            const double *L, int64_t ld, int r0, int j0, int kk,
+                                            int lane) {
+    const int sidx = n % STAGES;
+    const uint32_t use = n / STAGES;
+    if (use > 0) mbar_wait(&empty[sidx], (use - 1) & 1);
+    double *sb = stage + sidx * (A_STAGE + B_STAGE);
+    if (lane == 0) mbar_expect_tx(&full[sidx], STAGE_BYTES);
+    __syncwarp();
+    if (lane < KC) {
+        bulk_g2s(sb + lane * AS, L + (size_t)(kk + lane) * ld + r0, MT * sizeof(double), &full[sidx]);
+    } else {
+        const int q = lane - KC;
+        bulk_g2s(sb + A_STAGE + q * BS, L + (size_t)(kk + q) * ld + j0, NB * sizeof(double), &full[sidx]);
     }
-    __device__ __forceinline__ void load(double *stage, int kk) const {
-        const size_t off = (size_t)kk * ld;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            cp_async16(stage + sa + i * 4 * AS, na ? ga + off + (size_t)(4 * i) * ld : ga, na);
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-            cp_async16(stage + sb + i * 8 * BS, nb ? gb + off + (size_t)(8 * i) * ld : gb, nb);
-    }
-};
+}
 
 __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
-    extern __shared__ __align__(16) double smem[];
+    extern __shared__ __align__(128) double smem[];
     double *stage = smem;
     double *LJ = smem;                  // diagonal block [r][c], aliases the stages
     double *Bt = smem + STAGE_DBL;      // Bt[q*BS + n] = Linv[n][q]
@@ -131,6 +153,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     double *cv = cy + NB;
     double *dg = cv + NB;               // sqrt pivots of the diagonal block
     double *red = dg + NB;              // per-warp partial sums
+    __shared__ __align__(8) uint64_t full[STAGES];
+    __shared__ __align__(8) uint64_t empty[STAGES];
     __shared__ int s_item;
     __shared__ int s_fail;
 
@@ -138,6 +162,16 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     double *L = a.work + (size_t)blockIdx.x * a.slot_stride;
+
+    if (tid == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NWARP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t pc = 0;  // operand chunks consumed so far (identical in every thread)
 
     for (;;) {
         if (tid == 0) s_item = (int)atomicAdd(a.counter, 1u);
@@ -166,6 +200,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             const int jw = min(NB, k - j0);
             const int nrows = k + 1 - j0;  // rows j0..k (row k: bordered y)
             const int ntiles = (nrows + MT - 1) / MT;
+            const int nk = j0 / KC;        // operand chunks per tile
+            const int npro = min(STAGES - 1, nk);
             for (int i = tid; i < NB; i += NT) {
                 const int cc = j0 + i;
                 const bool ok = cc < k;
@@ -173,53 +209,22 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 cy[i] = ok ? __ldg(ty + cc) : 0.0;
                 cv[i] = ok ? __ldg(tv + cc) : 0.0;
             }
+            // The previous block column's factor stores (generic proxy, made GPU-visible
+            // before the last barrier) are read next by bulk copies (async proxy); the
+            // stage memory was last touched by generic accesses (LJ, alpha).
+            if (warp == 0) {
+                fence_proxy_async();
+                for (int i = 0; i < npro; ++i)
+                    issue_chunk(pc + i, stage, full, empty, L, ld, j0, j0, i * KC, lane);
+            }
+            __syncthreads();  // cx/cy/cv visible
             for (int rt = 0; rt < ntiles; ++rt) {
                 const int r0 = j0 + rt * MT;
                 const int rbase = r0 + warp * 16;  // this warp's first row
                 double acc[2][8][2];
-#pragma unroll
-                for (int i = 0; i < 2; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-                // acc = L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
-                const int nk = j0 / KC;
-                if (nk > 0) {
-                    TileLoader ldr;
-                    ldr.init(L, ld, r0, k + 1, j0, k, tid);
-#pragma unroll
-                    for (int st = 0; st < STAGES - 1; ++st) {
-                        if (st < nk) ldr.load(stage + st * (A_STAGE + B_STAGE), st * KC);
-                        cp_async_commit();
-                    }
-                    for (int kc = 0; kc < nk; ++kc) {
-                        cp_async_wait<STAGES - 2>();
-                        __syncthreads();
-                        const int nxt = kc + STAGES - 1;
-                        if (nxt < nk) ldr.load(stage + (nxt % STAGES) * (A_STAGE + B_STAGE), nxt * KC);
-                        cp_async_commit();
-                        const double *As = stage + (kc % STAGES) * (A_STAGE + B_STAGE);
-                        const double *Bs = As + A_STAGE;
-#pragma unroll
-                        for (int k4 = 0; k4 < KC / 4; ++k4) {
-                            const double *ap = As + (k4 * 4 + t) * AS + warp * 16 + g;
-                            const double *bp = Bs + (k4 * 4 + t) * BS + g;
-                            double af[2], bf[8];
-                            af[0] = ap[0];
-                            af[1] = ap[8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j)
-#pragma unroll
-                                for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
-                        }
-                    }
-                    cp_async_wait<0>();
-                }
-                __syncthreads();  // stages free (LJ may alias them); cx/cy/cv visible
-
-                // C = A - acc, A generated on the fly (Eq.3 second line), in registers
+                // acc = -A[r0:r0+MT, j0:j0+NB] (Eq.3 second line), generated while
+                // the first operand chunks of the tile are in flight.
                 {
                     double rx[2], ry[2];
 #pragma unroll
@@ -246,12 +251,48 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                     const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
                                     av = exp(sqrt(dx * dx + dy * dy) * ninv);
                                 }
-                                acc[i][j][e] = av - acc[i][j][e];
+                                acc[i][j][e] = -av;
                             }
                 }
 
+                // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
+                for (int kc = 0; kc < nk; ++kc) {
+                    const uint32_t n = pc + kc;
+                    if (warp == 0 && kc + STAGES - 1 < nk)
+                        issue_chunk(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
+                                    (kc + STAGES - 1) * KC, lane);
+                    mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
+                    const double *As = stage + (n % STAGES) * (A_STAGE + B_STAGE);
+                    const double *Bs = As + A_STAGE;
+#pragma unroll
+                    for (int k4 = 0; k4 < KC / 4; ++k4) {
+                        const double *ap = As + (k4 * 4 + t) * AS + warp * 16 + g;
+                        const double *bp = Bs + (k4 * 4 + t) * BS + g;
+                        double af[2], bf[8];
+                        af[0] = ap[0];
+                        af[1] = ap[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[n % STAGES]);
+                }
+                pc += nk;
+                // Columns past the matrix (last block column) came from rows of the
+                // workspace beyond the factor: force C = 0 there (Linv^T is 0 there too).
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (j0 + j * 8 + 2 * t + e >= k) acc[0][j][e] = acc[1][j][e] = 0.0;
+
                 if (rt == 0) {
-                    // Diagonal block to SMEM, then fused unblocked Cholesky + inverse.
+                    __syncthreads();  // every warp is past the update: LJ may reuse the stages
+                    // Diagonal block C = -acc to SMEM, then fused unblocked Cholesky + inverse.
                     if (warp < NB / 16) {
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
@@ -261,7 +302,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 for (int e = 0; e < 2; ++e) {
                                     const int rl = warp * 16 + i * 8 + g;
                                     const int nl = j * 8 + 2 * t + e;
-                                    if (nl <= rl) LJ[rl * LJS + nl] = acc[i][j][e];
+                                    if (nl <= rl) LJ[rl * LJS + nl] = -acc[i][j][e];
                                 }
                     }
                     for (int e = tid; e < BT_DBL; e += NT) Bt[e] = 0.0;
@@ -301,15 +342,22 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         if (rr >= cc)
                             L[(size_t)(j0 + cc) * ld + j0 + rr] = rr == cc ? dg[cc] : LJ[rr * LJS + cc];
                     }
+                    __syncthreads();  // LJ (stage memory) dead from here on
                 }
 
-                // X = C . Linv^T (triangular solve against L_jj^T as a GEMM).  The A
-                // fragment for k-slice sl (columns 4sl..4sl+3) of row block i is
-                // C[g][4sl + t], held by lane 4g + 2(sl&1) + t/2 as element t&1 of
-                // acc[i][sl/2].  (Rows of the diagonal block itself are discarded: L_jj
-                // was stored above.)
-                // Two passes of 32 output columns keep C (64 registers) plus one half of X
-                // (32 registers) live, within the 128-register budget of 2 CTAs per SM.
+                // Prefetch the next row tile's first chunks (same block column: they read
+                // only earlier block columns) so their latency hides behind the TRSM.
+                if (rt + 1 < ntiles && warp == 0) {
+                    fence_proxy_async();
+                    for (int i = 0; i < npro; ++i)
+                        issue_chunk(pc + i, stage, full, empty, L, ld, r0 + MT, j0, i * KC, lane);
+                }
+
+                // X = C . Linv^T = -(acc . Linv^T) (triangular solve against L_jj^T as a
+                // GEMM).  The A fragment for k-slice sl (columns 4sl..4sl+3) of row block i
+                // is acc[g][4sl + t], held by lane 4g + 2(sl&1) + t/2 as element t&1 of
+                // acc[i][sl/2].  Two passes of 32 output columns keep C (64 registers) plus
+                // one half of X (32 registers) live, within the 128-register budget.
                 const int rskip = rt == 0 ? j0 + jw : 0;  // first row below L_jj
                 const int src_lo = (g << 2) + (t >> 1);
                 const bool odd = t & 1;
@@ -351,17 +399,17 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 const int r = rbase + i * 8 + g;
                                 const int nl = h * 32 + j * 8 + 2 * t + e;
                                 if (nl < jw && r <= k && r >= rskip)
-                                    L[(size_t)(j0 + nl) * ld + r] = xo[i][j][e];
+                                    L[(size_t)(j0 + nl) * ld + r] = -xo[i][j][e];
                             }
                 }
                 if (rt == ntiles - 1) {
-                    // The factor columns just written are re-read through L2 only
-                    // (cp.async.cg, ld.global.cg) by other threads of this CTA in later
-                    // block columns and in the back-substitution: make them visible at GPU
-                    // scope (L2) before the barrier, not just at CTA scope (L1).
+                    // The factor columns just written are re-read through L2 only (bulk
+                    // copies, ld.global.cg) by other threads of this CTA in later block
+                    // columns and in the back-substitution: make them visible at GPU
+                    // scope before the barrier.
                     __threadfence();
+                    __syncthreads();
                 }
-                __syncthreads();
             }
         }
 
@@ -457,8 +505,9 @@ size_t cv_kernel_smem_bytes() { return SMEM_BYTES; }
 int cv_kernel_max_k() { return 1 << 20; }  // bounded by the factor workspace, not SMEM
 size_t cv_kernel_slot_doubles(int64_t kmax) {
     // factor (ld x k) + alpha when it does not fit in SMEM
-    // (rounded to 256 B: every slot base must keep the 16-B alignment cp.async needs)
-    const size_t d = (size_t)factor_ld(kmax) * (size_t)(kmax > 0 ? kmax : 1) + (size_t)kmax;
+    // + MT doubles: a bulk copy of the last column's row tile may read past row k.
+    // Rounded to 256 B: every slot base keeps the 16-B alignment bulk copies need.
+    const size_t d = (size_t)factor_ld(kmax) * (size_t)(kmax > 0 ? kmax : 1) + (size_t)kmax + MT;
     return (d + 31) / 32 * 32;
 }
 
