@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpgpcv.so")
+LIB_PATH = os.environ.get("PGPCV_LIB") or os.path.join(_HERE, "libpgpcv.so")
 
 OK, EINVAL, ENUMERIC, EEMPTY, ECUDA, ENOMEM, ENCCL, ESTATE = 0, -2, -3, -4, -5, -6, -7, -8
 ERROR_NAMES = {EINVAL: "EINVAL", ENUMERIC: "ENUMERIC", EEMPTY: "EEMPTY", ECUDA: "ECUDA",

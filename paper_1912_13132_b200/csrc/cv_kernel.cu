@@ -14,8 +14,13 @@
 // cross-covariance is generated where it is consumed, from the subset's staged
 // coordinates (distance -> exp), so a config costs no HBM traffic beyond the factor L.
 //
-// Data layout (per resident CTA, in HBM): L is column-major with leading dimension
-// ld = roundup(k+1, 16) doubles; rows 0..k-1 hold the Cholesky factor, row k holds z.
+// Data layout (per resident CTA, in HBM): L has k+1 rows (rows 0..k-1 the Cholesky factor,
+// row k the bordered z) and k columns, stored in column groups of KC = 16: group q holds
+// rows 0..ld-1 (ld = roundup(k+1, 16)) with each row's 16 values contiguous (128 B) and
+// XOR-swizzled by the row,  L(r, c) at ((c>>4)*ld + r)*16 + ((c & 15) ^ 4(r & 3)).
+// An operand chunk (MT or NB consecutive rows of one column group) is then one
+// contiguous 16 KB / 8 KB block: one bulk copy, and conflict-free DMMA fragment loads
+// from the unpadded SMEM image.
 //
 // Left-looking step for block column j (width NB = 64, columns j0..j0+jw-1), for every
 // row tile of MT = 128 rows r0.. (rows j0..k):
@@ -23,8 +28,9 @@
 //            the tile's first operand chunks are in flight
 //   acc   += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T       -- FP64 DMMA (mma.m8n8k4),
 //            operands streamed HBM/L2 -> SMEM by 1-D bulk copies (cp.async.bulk, one
-//            column of the tile per copy) issued by warp 0, 3 stages of KC = 16 columns
-//            tracked by full/empty mbarriers (no CTA-wide barrier in the loop)
+//            16 KB + one 8 KB copy per chunk of KC = 16 columns) issued by one thread,
+//            3 SMEM stages tracked by full/empty mbarriers (no CTA-wide barrier in the
+//            loop) plus L2 prefetches (cp.async.bulk.prefetch.L2) PFD chunks further ahead
 //   C      = -acc
 //   tile 0 : L_jj = chol(C[0:jw, 0:jw]) and Linv = L_jj^{-1}, fused, in SMEM
 //   X      = C . Linv^T                                      -- FP64 DMMA; the A operand
@@ -32,9 +38,7 @@
 //   L[r0:, j0:j0+jw] = X   (tile 0: its first jw rows are L_jj itself)
 //
 // Each warp owns 16 full rows of a tile (8 warps x 16 = 128), so the TRSM needs no
-// cross-warp exchange.  SMEM operand tiles are k-major with a row stride of MT+4 / NB+4
-// doubles: a stride of 8 (mod 32) 4-byte words makes the DMMA fragment loads (lane (g,t)
-// reads element [t][g]) conflict-free per half-warp.  113.7 KB of SMEM and <= 128
+// cross-warp exchange.  110.7 KB of SMEM and <= 128
 // registers per thread let two CTAs share an SM, so one CTA's barriers, epilogue,
 // diagonal factorization and back-substitution overlap the other's DMMA stream.
 #include <cmath>
@@ -49,14 +53,17 @@ constexpr int MT = kMT;
 constexpr int NB = kNB;
 constexpr int NT = kThreads;
 constexpr int NWARP = NT / 32;
-constexpr int KC = 16;
+constexpr int KC = 16;       // = the column-group width of the factor layout
 constexpr int STAGES = 3;
-constexpr int AS = MT + 4;  // 132 doubles = 264 words == 8 (mod 32)
-constexpr int BS = NB + 4;  // 68 doubles  = 136 words == 8 (mod 32)
-constexpr int LJS = NB + 1; // 65: row stride of the diagonal block in SMEM
-constexpr int A_STAGE = KC * AS;
-constexpr int B_STAGE = KC * BS;
-constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE);  // 9,600 doubles
+#ifndef PGPCV_PFD
+#define PGPCV_PFD 4
+#endif
+constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (chunks)
+constexpr int BS = NB + 4;   // 68 doubles = 136 words == 8 (mod 32): Linv^T rows
+constexpr int LJS = NB + 1;  // 65: row stride of the diagonal block in SMEM
+constexpr int A_STAGE = MT * KC;                         // 2,048 doubles (16 KB)
+constexpr int B_STAGE = NB * KC;                         // 1,024 doubles (8 KB)
+constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE);  // 9,216 doubles
 constexpr int BT_DBL = NB * BS;                          // Linv^T tile
 constexpr int COL_DBL = 3 * NB;                          // block-column x, y, value
 constexpr int MISC_DBL = NB + NWARP;                     // sqrt pivots, warp partials
@@ -64,7 +71,7 @@ constexpr size_t SMEM_BYTES = sizeof(double) * (STAGE_DBL + BT_DBL + COL_DBL + M
 static_assert(NB * LJS <= STAGE_DBL, "diagonal block must fit in the stage buffers");
 static_assert(NB * LJS <= BT_DBL, "back-substitution block must fit in the Linv buffer");
 static_assert(SMEM_BYTES <= 115712, "two CTAs per SM");
-static_assert((AS * 2) % 32 == 8 && (BS * 2) % 32 == 8, "fragment-load strides");
+static_assert((BS * 2) % 32 == 8, "fragment-load stride of Linv^T");
 static_assert(MT == 16 * NWARP && NB == 64, "each warp owns 16 rows x 64 columns");
 
 // ---------------------------------------------------------------- mbarrier / bulk copy
@@ -120,27 +127,45 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));  // 24,576 B
 
-// Operand chunk n of the running sequence (stage n % STAGES, use n / STAGES): warp 0
-// waits until every warp released the stage's previous use, then its 32 lanes each
-// issue one bulk copy -- lanes 0..15 the A columns (MT doubles), 16..31 the B columns
-// (NB doubles) -- for columns kk..kk+KC-1 of the factor.  Rows past the matrix are
-// copied as whatever the workspace holds; they only reach discarded outputs (see the
-// masking of acc after the update).
+// Element (r, c) of the factor in the column-group tiled, row-swizzled layout.
+__device__ __forceinline__ size_t lidx(int64_t ld, int r, int c) {
+    return ((size_t)(c >> 4) * ld + r) * KC + ((c & 15) ^ ((r & 3) << 2));
+}
+// Start of the contiguous chunk rows r.. of column group q.
+__device__ __forceinline__ const double *lchunk(const double *L, int64_t ld, int q, int r) {
+    return L + ((size_t)q * ld + r) * KC;
+}
+
+// Operand chunk n of the running sequence (stage n % STAGES, use n / STAGES): one thread
+// waits until every warp released the stage's previous use, then issues two bulk copies:
+// rows r0..r0+MT-1 (A) and j0..j0+NB-1 (B) of column group kk/16.  Rows past the matrix
+// are copied as whatever the workspace holds; they only reach discarded outputs (see the
+// masking of acc after the update).  Chunk n + PFD is prefetched into L2.
 __device__ __forceinline__ void issue_chunk(uint32_t n, double *stage, uint64_t *full, uint64_t *empty,
-                                            const double *L, int64_t ld, int r0, int j0, int kk,
-                                            int lane) {
+                                            const double *L, int64_t ld, int r0, int j0, int kk) {
     const int sidx = n % STAGES;
     const uint32_t use = n / STAGES;
     if (use > 0) mbar_wait(&empty[sidx], (use - 1) & 1);
     double *sb = stage + sidx * (A_STAGE + B_STAGE);
-    if (lane == 0) mbar_expect_tx(&full[sidx], STAGE_BYTES);
-    __syncwarp();
-    if (lane < KC) {
-        bulk_g2s(sb + lane * AS, L + (size_t)(kk + lane) * ld + r0, MT * sizeof(double), &full[sidx]);
-    } else {
-        const int q = lane - KC;
-        bulk_g2s(sb + A_STAGE + q * BS, L + (size_t)(kk + q) * ld + j0, NB * sizeof(double), &full[sidx]);
-    }
+    mbar_expect_tx(&full[sidx], STAGE_BYTES);
+    bulk_g2s(sb, lchunk(L, ld, kk / KC, r0), MT * KC * sizeof(double), &full[sidx]);
+    bulk_g2s(sb + A_STAGE, lchunk(L, ld, kk / KC, j0), NB * KC * sizeof(double), &full[sidx]);
+}
+__device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int r0, int j0, int kk) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lchunk(L, ld, kk / KC, r0)),
+                 "r"((unsigned)(MT * KC * sizeof(double)))
+                 : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lchunk(L, ld, kk / KC, j0)),
+                 "r"((unsigned)(NB * KC * sizeof(double)))
+                 : "memory");
+}
+// Tile prologue: SMEM chunks 0..STAGES-2 and L2 prefetches of the next PFD chunks.
+__device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage, uint64_t *full,
+                                              uint64_t *empty, const double *L, int64_t ld, int r0,
+                                              int j0) {
+    fence_proxy_async();
+    for (int i = 0; i < min(STAGES - 1, nk); ++i) issue_chunk(pc + i, stage, full, empty, L, ld, r0, j0, i * KC);
+    for (int i = STAGES - 1; i < min(STAGES - 1 + PFD, nk); ++i) prefetch_chunk(L, ld, r0, j0, i * KC);
 }
 
 __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
@@ -201,7 +226,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             const int nrows = k + 1 - j0;  // rows j0..k (row k: bordered y)
             const int ntiles = (nrows + MT - 1) / MT;
             const int nk = j0 / KC;        // operand chunks per tile
-            const int npro = min(STAGES - 1, nk);
             for (int i = tid; i < NB; i += NT) {
                 const int cc = j0 + i;
                 const bool ok = cc < k;
@@ -212,11 +236,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             // The previous block column's factor stores (generic proxy, made GPU-visible
             // before the last barrier) are read next by bulk copies (async proxy); the
             // stage memory was last touched by generic accesses (LJ, alpha).
-            if (warp == 0) {
-                fence_proxy_async();
-                for (int i = 0; i < npro; ++i)
-                    issue_chunk(pc + i, stage, full, empty, L, ld, j0, j0, i * KC, lane);
-            }
+            if (tid == 0) tile_prologue(pc, nk, stage, full, empty, L, ld, j0, j0);
+            __syncwarp();
             __syncthreads();  // cx/cy/cv visible
             for (int rt = 0; rt < ntiles; ++rt) {
                 const int r0 = j0 + rt * MT;
@@ -256,28 +277,39 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 }
 
                 // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
+                const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
-                    if (warp == 0 && kc + STAGES - 1 < nk)
-                        issue_chunk(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
-                                    (kc + STAGES - 1) * KC, lane);
+                    if (tid == 0) {
+                        if (kc + STAGES - 1 < nk)
+                            issue_chunk(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
+                                        (kc + STAGES - 1) * KC);
+                        if (kc + STAGES - 1 + PFD < nk)
+                            prefetch_chunk(L, ld, r0, j0, (kc + STAGES - 1 + PFD) * KC);
+                    }
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
+                    __syncwarp();  // mma.sync.aligned needs the whole warp converged
                     const double *As = stage + (n % STAGES) * (A_STAGE + B_STAGE);
-                    const double *Bs = As + A_STAGE;
+                    const double *ap = As + (warp * 16 + g) * KC + t;
+                    const double *bp = As + A_STAGE + g * KC + t;
 #pragma unroll
                     for (int k4 = 0; k4 < KC / 4; ++k4) {
-                        const double *ap = As + (k4 * 4 + t) * AS + warp * 16 + g;
-                        const double *bp = Bs + (k4 * 4 + t) * BS + g;
+                        const int o = (k4 << 2) ^ sw;
                         double af[2], bf[8];
-                        af[0] = ap[0];
-                        af[1] = ap[8];
+                        af[0] = ap[o];
+                        af[1] = ap[8 * KC + o];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8];
+                        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * KC + o];
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
 #pragma unroll
                             for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
                     }
+                    // Release the stage: this warp's generic-proxy reads of it must be
+                    // ordered before the async-proxy bulk copy that will refill it (the
+                    // mbarrier alone orders only within the generic proxy; without this
+                    // fence stale/partial operands were observed at ~1e-3 of items).
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[n % STAGES]);
                 }
@@ -338,20 +370,18 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     }
                     // L_jj -> the factor (lower triangle; the diagonal from the pivots)
                     for (int e = tid; e < jw * jw; e += NT) {
-                        const int cc = e / jw, rr = e % jw;
+                        const int rr = e / jw, cc = e % jw;
                         if (rr >= cc)
-                            L[(size_t)(j0 + cc) * ld + j0 + rr] = rr == cc ? dg[cc] : LJ[rr * LJS + cc];
+                            L[lidx(ld, j0 + rr, j0 + cc)] = rr == cc ? dg[cc] : LJ[rr * LJS + cc];
                     }
-                    __syncthreads();  // LJ (stage memory) dead from here on
+                    fence_proxy_async();  // generic LJ accesses before bulk copies refill it
+                    __syncthreads();      // LJ (stage memory) dead from here on
                 }
 
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
-                if (rt + 1 < ntiles && warp == 0) {
-                    fence_proxy_async();
-                    for (int i = 0; i < npro; ++i)
-                        issue_chunk(pc + i, stage, full, empty, L, ld, r0 + MT, j0, i * KC, lane);
-                }
+                if (rt + 1 < ntiles && tid == 0) tile_prologue(pc, nk, stage, full, empty, L, ld, r0 + MT, j0);
+                __syncwarp();
 
                 // X = C . Linv^T = -(acc . Linv^T) (triangular solve against L_jj^T as a
                 // GEMM).  The A fragment for k-slice sl (columns 4sl..4sl+3) of row block i
@@ -399,15 +429,16 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 const int r = rbase + i * 8 + g;
                                 const int nl = h * 32 + j * 8 + 2 * t + e;
                                 if (nl < jw && r <= k && r >= rskip)
-                                    L[(size_t)(j0 + nl) * ld + r] = -xo[i][j][e];
+                                    L[lidx(ld, r, j0 + nl)] = -xo[i][j][e];
                             }
                 }
                 if (rt == ntiles - 1) {
-                    // The factor columns just written are re-read through L2 only (bulk
-                    // copies, ld.global.cg) by other threads of this CTA in later block
-                    // columns and in the back-substitution: make them visible at GPU
-                    // scope before the barrier.
+                    // The factor columns just written (generic proxy) are re-read by bulk
+                    // copies (async proxy) and ld.global.cg in later block columns and the
+                    // back-substitution: each writer makes its stores GPU-visible and orders
+                    // them before async-proxy accesses, then the barrier.
                     __threadfence();
+                    fence_proxy_async();
                     __syncthreads();
                 }
             }
@@ -422,23 +453,44 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         }
 
         // ---------------- backward substitution L^T alpha = z ----------------
-        double *alpha = k <= STAGE_DBL ? stage : L + (size_t)ld * k;  // SMEM when it fits
+        // alpha (k doubles) and the per-warp partial sums (NWARP x NB) live in the stage
+        // buffers when they fit, else alpha goes to the slot's scratch after the factor.
+        const bool alpha_smem = k + NWARP * NB <= STAGE_DBL;
+        double *alpha = alpha_smem ? stage : L + (size_t)((k + KC - 1) / KC) * ld * KC;
+        double *part2 = alpha_smem ? stage + STAGE_DBL - NWARP * NB : stage;
         double *LB = Bt;        // diagonal block, [row][col] stride LJS
         double *tvec = cx;      // NB
         for (int jb = nblk - 1; jb >= 0; --jb) {
             const int j0 = jb * NB;
             const int jw = min(NB, k - j0);
             const int rs = j0 + jw;
-            for (int cl = warp; cl < jw; cl += NWARP) {
-                const double *col = L + (size_t)(j0 + cl) * ld;
-                double sum = 0.0;
-                for (int r = rs + lane; r < k; r += 32) sum += __ldcg(col + r) * alpha[r];
-                sum = warp_sum(sum);
-                if (lane == 0) tvec[cl] = __ldcg(col + k) - sum;  // z_c - L[c+1:, c] . alpha
+            // partial t_c = sum_{r >= rs} L[r][c] alpha_r: warp w takes rows rs+w+8i, lane
+            // the logical columns 2 lane, 2 lane + 1 (4 contiguous 128-B rows per warp load)
+            {
+                const int c0 = 2 * lane;
+                const int grp = (j0 >> 4) + (c0 >> 4);
+                double p0 = 0.0, p1 = 0.0;
+                if (c0 < jw) {
+                    for (int r = rs + warp; r < k; r += NWARP) {
+                        const double ar = alpha[r];
+                        const double *row = L + ((size_t)grp * ld + r) * KC;
+                        const int sw = (r & 3) << 2;
+                        p0 += __ldcg(row + ((c0 & 15) ^ sw)) * ar;
+                        p1 += __ldcg(row + (((c0 + 1) & 15) ^ sw)) * ar;
+                    }
+                }
+                part2[warp * NB + c0] = p0;
+                part2[warp * NB + c0 + 1] = p1;
             }
             for (int e = tid; e < jw * jw; e += NT) {
-                const int cc = e / jw, rr = e % jw;  // column cc, row rr of the block
-                if (rr >= cc) LB[rr * LJS + cc] = __ldcg(L + (size_t)(j0 + cc) * ld + j0 + rr);
+                const int rr = e / jw, cc = e % jw;  // row rr, column cc of the block
+                if (rr >= cc) LB[rr * LJS + cc] = __ldcg(L + lidx(ld, j0 + rr, j0 + cc));
+            }
+            __syncthreads();
+            if (tid < jw) {
+                double sum = 0.0;
+                for (int w = 0; w < NWARP; ++w) sum += part2[w * NB + tid];
+                tvec[tid] = __ldcg(L + lidx(ld, k, j0 + tid)) - sum;  // z_c - L[c+1:, c] . alpha
             }
             __syncthreads();
             if (warp == 0) {
@@ -470,6 +522,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             part += e * e;
         }
         if (lane == 0) red[warp] = part;
+        fence_proxy_async();  // generic alpha/part2 accesses before the next item's bulk copies
         __syncthreads();
         if (tid == 0) {
             double l = 0.0;
@@ -504,10 +557,12 @@ __global__ void reduce_kernel(const double *subset_loss, const uint8_t *fail, in
 size_t cv_kernel_smem_bytes() { return SMEM_BYTES; }
 int cv_kernel_max_k() { return 1 << 20; }  // bounded by the factor workspace, not SMEM
 size_t cv_kernel_slot_doubles(int64_t kmax) {
-    // factor (ld x k) + alpha when it does not fit in SMEM
-    // + MT doubles: a bulk copy of the last column's row tile may read past row k.
-    // Rounded to 256 B: every slot base keeps the 16-B alignment bulk copies need.
-    const size_t d = (size_t)factor_ld(kmax) * (size_t)(kmax > 0 ? kmax : 1) + (size_t)kmax + MT;
+    // column groups x ld x 16 (the factor) + alpha when it does not fit in SMEM + MT x 16:
+    // a bulk copy of the last group's row tile may read past row k.  Rounded to 256 B so
+    // every slot base keeps the alignment bulk copies need.
+    const int64_t groups = (kmax + KC - 1) / KC;
+    const size_t d = (size_t)(groups > 0 ? groups : 1) * (size_t)factor_ld(kmax) * KC +
+                     (size_t)kmax + (size_t)MT * KC;
     return (d + 31) / 32 * 32;
 }
 

@@ -96,6 +96,22 @@ def test_cv_loss_c2_full_grid(ctx):
     _assert_close(res.loss, ref.loss)
 
 
+def test_repeated_runs_bit_identical_and_exact(ctx):
+    """Race regression: the full c2 grid three times -- every run within 1e-9 of the oracle
+    and bit-identical to the others (dynamic scheduling must not change any value).  A
+    missing cross-proxy fence in the operand pipeline once corrupted ~1e-3 of the items."""
+    w = wl("c2")
+    ref_part = _assert_partition_equal(ctx, w)
+    ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, w.params, threads=THREADS)
+    first = None
+    for _ in range(3):
+        res = ctx.cv_loss(w.params)
+        _assert_close(res.subset_loss, ref.subset_loss)
+        if first is None:
+            first = res.subset_loss.copy()
+        assert np.array_equal(res.subset_loss, first)
+
+
 def test_cv_loss_c3_configs(ctx):
     """All 1,600 subsets of c3 at the grid corners and the truth."""
     w = wl("c3")
