@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PGPCV_VERSION 1
+#define PGPCV_VERSION 2
 
 /* Error codes. */
 #define PGPCV_OK 0
@@ -86,7 +86,23 @@ typedef struct {
     int64_t n_empty_val; /* subsets with no validation data (loss 0, "ignored") */
     int64_t n_train;     /* points with role 0 */
     int64_t n_val;       /* points with role 1 */
+    int64_t n_test;      /* points with role 2 (each in exactly one core tile) */
+    int64_t max_test;    /* largest test subset */
 } pgpcv_partition_info;
+
+/* Outputs of pgpcv_evaluate: caller-owned host arrays, each NULL to skip it.  C = n_params,
+ * N = number of subsets.  Requesting loss or subset_loss runs the CV prediction (Eq.3-4);
+ * requesting nll or subset_nll adds the -2 log-likelihood (Eq.2) of every subset's
+ * training data from the same factorization (no second factorization). */
+typedef struct {
+    double *loss;        /* [C] C~V per config (Eq.7), summed over subsets in ascending s */
+    double *subset_loss; /* [N*C] subset-major SSPE z_{s,c}; exactly 0 when m_s = 0 (R10) */
+    int32_t *status;     /* [C] -1 ok, else the smallest subset whose factorization failed */
+    double *nll;         /* [C] sum over subsets of -2 log L_s (a composite likelihood) */
+    double *subset_nll;  /* [N*C] -2 log L_s = k log(2 pi) + log det(s2 Sigma + tau I)
+                            + y^T (s2 Sigma + tau I)^{-1} y over subset s's training data
+                            (Eq.2); 0 when k_s = 0 */
+} pgpcv_outputs;
 
 /* Device-side timing of the last pgpcv_cv_loss call (CUDA events on the ctx stream). */
 typedef struct {
@@ -181,7 +197,56 @@ int pgpcv_nccl_get_unique_id(void *out);
 int pgpcv_cv_loss(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, double *loss,
                   double *subset_loss, int32_t *status);
 
-/* Timing and work counts of the last successful pgpcv_cv_loss on ctx. */
+/* The general form of pgpcv_cv_loss (Alg.1 lines 4-9 plus row f3 of the scope table):
+ * one batched factorization per (owned subset, config) serves every requested output.
+ * Subsets enter the CV outputs when they have validation data; with nll/subset_nll
+ * requested every owned subset is factored (the likelihood needs no targets).  Across
+ * GPUs the [loss | nll] vector is all-reduced once (per-subset arrays, when requested,
+ * are all-reduced instead; each entry has one owner so the sums are exact).
+ * Errors: EINVAL (no output requested, bad params), ESTATE, EEMPTY (CV output requested
+ * but no validation data), ENUMERIC (loss/nll[c] = NaN and status[c] >= 0 for a non-PD
+ * config; others valid), ECUDA, ENOMEM, ENCCL. */
+int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params,
+                   const pgpcv_outputs *out);
+
+/* Grid-search consumer of the last CV evaluation (scope row f1).  Reads
+ * the per-subset losses left on the device by the last pgpcv_evaluate/pgpcv_cv_loss (which
+ * must have computed every subset: world 1, or subset_loss requested; else ESTATE).
+ * Outputs (host, caller-owned, each NULL to skip):
+ *   best:        int32[1] argmin_c loss[c] (zeta_hat_CV; ties -> lowest c; NaN
+ *                configs never win; -1 if every config failed)
+ *   rmspe:       double[C] global RMSPE sqrt(loss[c] / n_V)
+ *   local_best:  int32[N] argmin_c subset_loss[s, c] (ties -> lowest c; -1 when m_s = 0)
+ *   local_rmspe: double[N*C] sqrt(subset_loss[s, c] / m_s) (NaN when m_s = 0 or failed)
+ *   wins:        int32[C] number of subsets whose local best is c
+ * Errors: ESTATE, ECUDA. */
+int pgpcv_select(pgpcv_ctx *ctx, int32_t *best, double *rmspe, int32_t *local_best,
+                 double *local_rmspe, int32_t *wins);
+
+/* Kriging prediction of held-out points with a chosen configuration per subset (P:466-468:
+ * "the hold-out test data are predicted using the global zeta_hat_CV and using the best
+ * local parameter configuration for each subset").  For every owned subset s with targets,
+ * factor Sigma + lambda I of its training data y~^s_T under params[subset_config[s]]
+ * (params[0] for every subset when subset_config is NULL) and predict its core-tile points
+ * of role `target_role` (PGPCV_ROLE_TEST or PGPCV_ROLE_VALIDATION; with VALIDATION and one
+ * config this reproduces pgpcv_cv_loss).
+ *   yhat:        double[n_targets] or NULL: predictions in the target CSR order (subset-
+ *                major, ascending point index; see pgpcv_partition_export_test / _export)
+ *   subset_sspe: double[N] or NULL: sum of squared prediction errors per subset
+ *   sspe:        double[1] or NULL: their sum in ascending s (RMSPE = sqrt(sspe/n_targets))
+ * Errors: EINVAL (bad params / role / config index), ESTATE, ENUMERIC (sspe = NaN),
+ * ECUDA, ENOMEM, ENCCL. */
+int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params,
+                  const int32_t *subset_config, int32_t target_role, double *yhat,
+                  double *subset_sspe, double *sspe);
+
+/* CSR lists of the test points (role 2) per core tile: test_off int64[N+1], test_idx
+ * int32[n_test] (ascending point index within a subset).  Either may be NULL.
+ * Errors: ESTATE, ECUDA. */
+int pgpcv_partition_export_test(pgpcv_ctx *ctx, int64_t *test_off, int32_t *test_idx);
+
+/* Timing and work counts of the last successful pgpcv_cv_loss / pgpcv_evaluate /
+ * pgpcv_predict on ctx. */
 int pgpcv_last_timing(const pgpcv_ctx *ctx, pgpcv_timing *out);
 
 /* Host-only helper (no GPU needed): LPT assignment of n_items with costs cost[] to

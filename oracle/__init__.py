@@ -53,10 +53,11 @@ def _load():
             lib = ctypes.CDLL(_LIB)
             d, i32, i64, p = ctypes.c_double, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
             lib.oracle_edges.argtypes = [d, d, i32, p]
-            lib.oracle_partition_count.argtypes = [i64, p, p, p, d, d, d, d, i32, i32, d, p, p]
-            lib.oracle_partition_fill.argtypes = [i64, p, p, p, d, d, d, d, i32, i32, d, p, p, p, p]
+            u8 = ctypes.c_uint8
+            lib.oracle_partition_count.argtypes = [i64, p, p, p, d, d, d, d, i32, i32, d, u8, p, p]
+            lib.oracle_partition_fill.argtypes = [i64, p, p, p, d, d, d, d, i32, i32, d, u8, p, p, p, p]
             for f in (lib.oracle_subset_cv, lib.oracle_subset_cv_ld):
-                f.argtypes = [i64, p, p, p, i64, p, p, p, d, d, d, p]
+                f.argtypes = [i64, p, p, p, i64, p, p, p, d, d, d, p, p]
             lib.oracle_neg2loglik.argtypes = [i64, p, p, p, d, d, d, p]
             _lib = lib
     return _lib
@@ -107,9 +108,11 @@ class Partition:
         return self.val_idx[self.val_off[s]:self.val_off[s + 1]]
 
 
-def partition(x, y, role, domain, kx: int, ky: int, delta: float) -> Partition:
+def partition(x, y, role, domain, kx: int, ky: int, delta: float, core_role: int = 1) -> Partition:
     """Brute-force subset membership (Alg.1 lines 2-3; shell of width delta, P:154-159;
-    readings R1-R6).  Every point is tested against every tile interval on each axis."""
+    readings R1-R6).  Every point is tested against every tile interval on each axis.
+    ``core_role`` selects the points listed per core tile: 1 = validation (y^i_V), 2 = test
+    (the held-out points predicted with the chosen parameters)."""
     lib = _load()
     x = np.ascontiguousarray(x, np.float64)
     y = np.ascontiguousarray(y, np.float64)
@@ -120,7 +123,7 @@ def partition(x, y, role, domain, kx: int, ky: int, delta: float) -> Partition:
     vc = np.zeros(N, np.int64)
     xmin, xmax, ymin, ymax = (float(v) for v in domain)
     rc = lib.oracle_partition_count(n, _ptr(x), _ptr(y), _ptr(role), xmin, xmax, ymin, ymax,
-                                    kx, ky, float(delta), _ptr(tc), _ptr(vc))
+                                    kx, ky, float(delta), int(core_role), _ptr(tc), _ptr(vc))
     if rc:
         raise OracleError(rc, "partition")
     toff = np.zeros(N + 1, np.int64)
@@ -130,26 +133,29 @@ def partition(x, y, role, domain, kx: int, ky: int, delta: float) -> Partition:
     tidx = np.empty(int(toff[-1]), np.int32)
     vidx = np.empty(int(voff[-1]), np.int32)
     rc = lib.oracle_partition_fill(n, _ptr(x), _ptr(y), _ptr(role), xmin, xmax, ymin, ymax,
-                                   kx, ky, float(delta), _ptr(toff), _ptr(tidx), _ptr(voff),
-                                   _ptr(vidx))
+                                   kx, ky, float(delta), int(core_role), _ptr(toff), _ptr(tidx),
+                                   _ptr(voff), _ptr(vidx))
     if rc:
         raise OracleError(rc, "partition")
     return Partition(toff, tidx, voff, vidx, kx, ky)
 
 
 def subset_cv(tx, ty, tv, vx, vy, vv, range_: float, sigma2: float, nugget: float,
-              long_double: bool = False) -> float:
+              long_double: bool = False, return_yhat: bool = False):
     """CV(y~_T, y_V, zeta) of Eq.4 with Eq.3's predictor for one
-    subset and one (range, sigma^2, nugget).  Raises OracleError(ENUMERIC) if not PD."""
+    subset and one (range, sigma^2, nugget).  Raises OracleError(ENUMERIC) if not PD.
+    With ``return_yhat`` also returns the predictions yhat_v (Eq.3) as an array."""
     lib = _load()
     a = [np.ascontiguousarray(v, np.float64) for v in (tx, ty, tv, vx, vy, vv)]
     out = np.zeros(1, np.float64)
+    yhat = np.zeros(a[3].shape[0], np.float64)
     f = lib.oracle_subset_cv_ld if long_double else lib.oracle_subset_cv
     rc = f(a[0].shape[0], _ptr(a[0]), _ptr(a[1]), _ptr(a[2]), a[3].shape[0], _ptr(a[3]),
-           _ptr(a[4]), _ptr(a[5]), float(range_), float(sigma2), float(nugget), _ptr(out))
+           _ptr(a[4]), _ptr(a[5]), float(range_), float(sigma2), float(nugget), _ptr(out),
+           _ptr(yhat) if return_yhat else None)
     if rc:
         raise OracleError(rc, "subset_cv")
-    return float(out[0])
+    return (float(out[0]), yhat) if return_yhat else float(out[0])
 
 
 def neg2loglik(tx, ty, tv, range_: float, sigma2: float, nugget: float) -> float:
@@ -233,3 +239,94 @@ def subset_flops(k, m) -> float:
     m = np.asarray(m, np.float64)
     f = k ** 3 / 3 + k ** 2 / 2 + k / 6 + 2 * k ** 2 + 2 * m * k + 3 * m
     return np.where(m > 0, f, 0.0)
+
+
+def neg2loglik_all(x, y, v, part: Partition, params, subsets=None, threads: int | None = None):
+    """Row f3: per-subset -2 log-likelihood (Eq.2) of each subset's training data
+    y~^i_T, and their sum over subsets in ascending s (a composite likelihood; NaN when a
+    subset's covariance is not PD).  Returns (total[C], per_subset[N, C])."""
+    params = np.asarray(params, np.float64).reshape(-1, 3)
+    C, N = params.shape[0], part.n_subsets
+    sub = np.arange(N) if subsets is None else np.asarray(subsets, np.int64)
+    res = np.full((N, C), np.nan)
+    tasks = [(int(s), c) for s in sub for c in range(C)]
+
+    def run(t):
+        s, c = t
+        ti = part.train(s)
+        try:
+            res[s, c] = neg2loglik(x[ti], y[ti], v[ti], *params[c])
+        except OracleError as e:
+            if e.code != ENUMERIC:
+                raise
+
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        list(ex.map(run, tasks))
+    total = np.zeros(C)
+    for c in range(C):
+        acc = 0.0
+        for s in sub:
+            acc = acc + float(res[s, c])
+        total[c] = acc
+    return total, res
+
+
+def select(loss, subset_loss, m):
+    """Row f1, the grid-search consumer, written out plainly:
+    best = argmin_c loss[c] (ties -> lowest c, NaN never wins); global RMSPE
+    sqrt(loss / n_V); local RMSPE sqrt(z_{s,c} / m_s); local best argmin_c z_{s,c}
+    (-1 when m_s = 0); wins[c] = number of subsets whose local best is c."""
+    loss = np.asarray(loss, np.float64)
+    subset_loss = np.asarray(subset_loss, np.float64)
+    m = np.asarray(m, np.int64)
+    N, C = subset_loss.shape
+    n_v = int(m.sum())
+    best, bl = -1, None
+    for c in range(C):
+        if not math.isnan(loss[c]) and (best < 0 or loss[c] < bl):
+            best, bl = c, loss[c]
+    rmspe = np.array([math.sqrt(loss[c] / n_v) if not math.isnan(loss[c]) else math.nan for c in range(C)])
+    local_best = np.full(N, -1, np.int32)
+    local_rmspe = np.full((N, C), np.nan)
+    wins = np.zeros(C, np.int32)
+    for s in range(N):
+        if m[s] == 0:
+            continue
+        b, bz = -1, None
+        for c in range(C):
+            z = subset_loss[s, c]
+            if math.isnan(z):
+                continue
+            local_rmspe[s, c] = math.sqrt(z / m[s])
+            if b < 0 or z < bz:
+                b, bz = c, z
+        local_best[s] = b
+        if b >= 0:
+            wins[b] += 1
+    return best, rmspe, local_best, local_rmspe, wins
+
+
+def predict(x, y, v, part: Partition, params, subset_config=None, threads: int | None = None):
+    """Kriging prediction of each subset's core-tile targets (``part`` built with
+    core_role=2 for the test points) with params[subset_config[s]].  Returns
+    (sspe total in ascending s, per-subset sspe[N], yhat in the target CSR order)."""
+    params = np.asarray(params, np.float64).reshape(-1, 3)
+    N = part.n_subsets
+    cfg = np.zeros(N, np.int64) if subset_config is None else np.asarray(subset_config, np.int64)
+    sub = np.zeros(N)
+    yhat = np.zeros(int(part.val_off[-1]))
+
+    def run(s):
+        ti, vi = part.train(s), part.val(s)
+        if vi.size == 0:
+            return
+        l, yh = subset_cv(x[ti], y[ti], v[ti], x[vi], y[vi], v[vi], *params[cfg[s]], return_yhat=True)
+        sub[s] = l
+        yhat[part.val_off[s]:part.val_off[s + 1]] = yh
+
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        list(ex.map(run, range(N)))
+    total = 0.0
+    for s in range(N):
+        total = total + float(sub[s])
+    return total, sub, yhat

@@ -89,11 +89,13 @@ static int check_inputs(int64_t n, const double *x, const double *y, const uint8
 }
 
 /* Pass 1: per-subset counts.  Subset id s = iy*kx + ix (reading R5).
- * train(s) = {p : role 0, p in the dilated tile s};  val(s) = {p : role 1, core(p) = s}
- * (reading R6: validation never comes from the shell; Eq.7 writes y^i_V). */
+ * train(s) = {p : role 0, p in the dilated tile s};  val(s) = {p : role core_role,
+ * core(p) = s} -- core_role 1 gives the validation lists (reading R6: validation never
+ * comes from the shell; Eq.7 writes y^i_V), core_role 2 the test lists predicted
+ * with the chosen parameters. */
 int oracle_partition_count(int64_t n, const double *x, const double *y, const uint8_t *role,
                            double xmin, double xmax, double ymin, double ymax,
-                           int32_t kx, int32_t ky, double delta,
+                           int32_t kx, int32_t ky, double delta, uint8_t core_role,
                            int64_t *train_cnt, int64_t *val_cnt) {
     int rc = check_inputs(n, x, y, role, xmin, xmax, ymin, ymax, kx, ky, delta);
     if (rc) return rc;
@@ -105,7 +107,7 @@ int oracle_partition_count(int64_t n, const double *x, const double *y, const ui
     int64_t N = (int64_t)kx * ky;
     for (int64_t s = 0; s < N; ++s) { train_cnt[s] = 0; val_cnt[s] = 0; }
     for (int64_t p = 0; p < n; ++p) {
-        if (role[p] == 1) {
+        if (role[p] == core_role) {
             int32_t ix = core_index(x[p], ex, kx), iy = core_index(y[p], ey, ky);
             val_cnt[(int64_t)iy * kx + ix] += 1;
         } else if (role[p] == 0) {
@@ -125,7 +127,7 @@ int oracle_partition_count(int64_t n, const double *x, const double *y, const ui
  * exclusive prefix sums of the pass-1 counts (N+1 entries, computed by the caller). */
 int oracle_partition_fill(int64_t n, const double *x, const double *y, const uint8_t *role,
                           double xmin, double xmax, double ymin, double ymax,
-                          int32_t kx, int32_t ky, double delta,
+                          int32_t kx, int32_t ky, double delta, uint8_t core_role,
                           const int64_t *train_off, int32_t *train_idx,
                           const int64_t *val_off, int32_t *val_idx) {
     int rc = check_inputs(n, x, y, role, xmin, xmax, ymin, ymax, kx, ky, delta);
@@ -139,7 +141,7 @@ int oracle_partition_fill(int64_t n, const double *x, const double *y, const uin
     if (rc) { free(ex); free(ey); free(tpos); free(vpos); return rc; }
     for (int64_t s = 0; s < N; ++s) { tpos[s] = train_off[s]; vpos[s] = val_off[s]; }
     for (int64_t p = 0; p < n; ++p) {
-        if (role[p] == 1) {
+        if (role[p] == core_role) {
             int32_t ix = core_index(x[p], ex, kx), iy = core_index(y[p], ey, ky);
             int64_t s = (int64_t)iy * kx + ix;
             val_idx[vpos[s]++] = (int32_t)p;
@@ -166,7 +168,7 @@ int oracle_partition_fill(int64_t n, const double *x, const double *y, const uin
 #define DEFINE_SUBSET_CV(NAME, REAL, EXP, SQRT)                                                    \
 int NAME(int64_t k, const double *tx, const double *ty, const double *tv,                          \
          int64_t m, const double *vx, const double *vy, const double *vv,                          \
-         double range, double sigma2, double nugget, double *loss_out) {                           \
+         double range, double sigma2, double nugget, double *loss_out, double *yhat_out) {         \
     if (!(range > 0) || !(sigma2 > 0) || !(nugget >= 0) || isinf(range) || isinf(sigma2) ||        \
         isinf(nugget))                                                                             \
         return OR_EINVAL;                                                                          \
@@ -226,6 +228,7 @@ int NAME(int64_t k, const double *tx, const double *ty, const double *tv,       
             REAL d = SQRT(dx * dx + dy * dy);                                                      \
             yhat += EXP(-d / theta) * alpha[j];                                                    \
         }                                                                                          \
+        if (yhat_out) yhat_out[v] = (double)yhat;                                                  \
         REAL e = yhat - (REAL)vv[v];                                                               \
         loss += e * e;                                                                             \
     }                                                                                              \

@@ -31,7 +31,10 @@ MAX_K = 19200
 EXPORTED = ("pgpcv_version", "pgpcv_create", "pgpcv_destroy", "pgpcv_last_error",
             "pgpcv_set_stream", "pgpcv_partition", "pgpcv_partition_device",
             "pgpcv_partition_export", "pgpcv_shard", "pgpcv_nccl_get_unique_id",
-            "pgpcv_cv_loss", "pgpcv_last_timing", "pgpcv_lpt_assign")
+            "pgpcv_cv_loss", "pgpcv_evaluate", "pgpcv_select", "pgpcv_predict",
+            "pgpcv_partition_export_test", "pgpcv_last_timing", "pgpcv_lpt_assign")
+ROLE_TRAIN, ROLE_VALIDATION, ROLE_TEST = 0, 1, 2
+ABI_VERSION = 2
 
 
 class PgpcvError(RuntimeError):
@@ -51,10 +54,16 @@ class Param(ctypes.Structure):
 
 class PartitionInfo(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in ("n_subsets", "sum_k", "sum_m", "max_k", "max_m",
-                                               "n_empty_val", "n_train", "n_val")]
+                                               "n_empty_val", "n_train", "n_val", "n_test",
+                                               "max_test")]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+class Outputs(ctypes.Structure):
+    """pgpcv_outputs: host output pointers (NULL to skip)."""
+    _fields_ = [(f, ctypes.c_void_p) for f in ("loss", "subset_loss", "status", "nll", "subset_nll")]
 
 
 class Timing(ctypes.Structure):
@@ -92,6 +101,10 @@ def load_library():
     lib.pgpcv_shard.argtypes = [p, ctypes.c_int, ctypes.c_int, p]
     lib.pgpcv_nccl_get_unique_id.argtypes = [p]
     lib.pgpcv_cv_loss.argtypes = [p, ctypes.POINTER(Param), i32, p, p, p]
+    lib.pgpcv_evaluate.argtypes = [p, ctypes.POINTER(Param), i32, ctypes.POINTER(Outputs)]
+    lib.pgpcv_select.argtypes = [p, p, p, p, p, p]
+    lib.pgpcv_predict.argtypes = [p, ctypes.POINTER(Param), i32, p, i32, p, p, p]
+    lib.pgpcv_partition_export_test.argtypes = [p, p, p]
     lib.pgpcv_last_timing.argtypes = [p, ctypes.POINTER(Timing)]
     lib.pgpcv_lpt_assign.argtypes = [i64, p, i32, p]
     for name in EXPORTED:
@@ -134,6 +147,25 @@ class CvResult:
     subset_loss: np.ndarray | None  # [N, C] per-subset SSPE z_i, or None
     status: np.ndarray        # [C] -1 ok, else first non-PD subset
     code: int                 # OK or ENUMERIC
+    nll: np.ndarray | None = None         # [C] sum_s -2 log L_s (Eq.2 per subset)
+    subset_nll: np.ndarray | None = None  # [N, C]
+
+
+@dataclass
+class Selection:
+    best: int                 # argmin_c loss[c] (zeta_hat_CV), -1 if every config failed
+    rmspe: np.ndarray         # [C] global RMSPE sqrt(loss / n_V)
+    local_best: np.ndarray    # [N] per-subset argmin_c (-1 when no validation data)
+    local_rmspe: np.ndarray   # [N, C]
+    wins: np.ndarray          # [C] subsets won per config
+
+
+@dataclass
+class Prediction:
+    sspe: float               # sum of squared prediction errors over all targets
+    subset_sspe: np.ndarray   # [N]
+    yhat: np.ndarray | None   # [n_targets] in target CSR order
+    code: int                 # OK or ENUMERIC
 
 
 class Context:
@@ -147,6 +179,7 @@ class Context:
             raise PgpcvError(rc, self._lib.pgpcv_last_error(None).decode())
         self._h = h
         self.info: dict | None = None
+        self._last_C = 0  # configs of the last CV evaluation (the shape pgpcv_select returns)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -231,7 +264,79 @@ class Context:
                                      _ptr(status))
         if rc not in (OK, ENUMERIC):
             self._check(rc, "pgpcv_cv_loss")
+        self._last_C = C
         return CvResult(loss, sub, status, rc)
+
+    def evaluate(self, params, loss: bool = True, subset_loss: bool = True, nll: bool = False,
+                 subset_nll: bool = False) -> CvResult:
+        """pgpcv_evaluate: CV loss and/or per-subset -2 log-likelihood from one factorization."""
+        params = np.ascontiguousarray(params, np.float64).reshape(-1, 3)
+        C = params.shape[0]
+        if self.info is None:
+            raise PgpcvError(ESTATE, "no partition")
+        N = self.info["n_subsets"]
+        par = (Param * C)(*[Param(*row) for row in params.tolist()])
+        arr = {"loss": np.empty(C) if loss else None,
+               "subset_loss": np.empty((N, C)) if subset_loss else None,
+               "status": np.empty(C, np.int32),
+               "nll": np.empty(C) if nll else None,
+               "subset_nll": np.empty((N, C)) if subset_nll else None}
+        out = Outputs(**{k: (v.ctypes.data if v is not None else None) for k, v in arr.items()})
+        rc = self._lib.pgpcv_evaluate(self._h, par, C, ctypes.byref(out))
+        if rc not in (OK, ENUMERIC):
+            self._check(rc, "pgpcv_evaluate")
+        self._last_C = C if (loss or subset_loss) else 0
+        return CvResult(arr["loss"], arr["subset_loss"], arr["status"], rc, arr["nll"], arr["subset_nll"])
+
+    def select(self) -> Selection:
+        """pgpcv_select on the last CV evaluation (grid-search consumer)."""
+        if self.info is None:
+            raise PgpcvError(ESTATE, "no partition")
+        N = self.info["n_subsets"]
+        C = self._last_C
+        if C <= 0:
+            raise PgpcvError(ESTATE, "pgpcv_select needs a preceding CV evaluation")
+        best = np.empty(1, np.int32)
+        rmspe = np.empty(C)
+        lb = np.empty(N, np.int32)
+        lr = np.empty((N, C))
+        wins = np.empty(C, np.int32)
+        self._check(self._lib.pgpcv_select(self._h, _ptr(best), _ptr(rmspe), _ptr(lb), _ptr(lr), _ptr(wins)),
+                    "pgpcv_select")
+        return Selection(int(best[0]), rmspe, lb, lr, wins)
+
+    def predict(self, params, subset_config=None, target_role: int = ROLE_TEST,
+                want_yhat: bool = True) -> Prediction:
+        """pgpcv_predict: kriging predictions of the targets with params[subset_config[s]]."""
+        params = np.ascontiguousarray(params, np.float64).reshape(-1, 3)
+        C = params.shape[0]
+        if self.info is None:
+            raise PgpcvError(ESTATE, "no partition")
+        N = self.info["n_subsets"]
+        par = (Param * C)(*[Param(*row) for row in params.tolist()])
+        cfg = None if subset_config is None else np.ascontiguousarray(subset_config, np.int32)
+        if cfg is not None and cfg.shape != (N,):
+            raise ValueError("subset_config must have one entry per subset")
+        n_t = self.info["n_test"] if target_role == ROLE_TEST else self.info["sum_m"]
+        yhat = np.empty(n_t) if want_yhat else None
+        sub = np.empty(N)
+        tot = np.empty(1)
+        rc = self._lib.pgpcv_predict(self._h, par, C, _ptr(cfg) if cfg is not None else None, int(target_role),
+                                     _ptr(yhat) if yhat is not None else None, _ptr(sub), _ptr(tot))
+        if rc not in (OK, ENUMERIC):
+            self._check(rc, "pgpcv_predict")
+        return Prediction(float(tot[0]), sub, yhat, rc)
+
+    def partition_export_test(self):
+        """(test_off, test_idx): CSR lists of the test points (role 2) per core tile."""
+        if self.info is None:
+            raise PgpcvError(ESTATE, "no partition")
+        N = self.info["n_subsets"]
+        off = np.empty(N + 1, np.int64)
+        idx = np.empty(self.info["n_test"], np.int32)
+        self._check(self._lib.pgpcv_partition_export_test(self._h, _ptr(off), _ptr(idx)),
+                    "pgpcv_partition_export_test")
+        return off, idx
 
     def last_timing(self) -> dict:
         t = Timing()

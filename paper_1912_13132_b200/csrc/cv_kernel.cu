@@ -217,7 +217,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         const double ninv = -1.0 / range;
         const int64_t ld = factor_ld(k);
         const int nblk = (k + NB - 1) / NB;
+        const int64_t oi = (int64_t)s * a.out_C + (a.out_C > 1 ? c : 0);  // output entry
         bool failed = false;
+        double logdet = 0.0;  // sum_i log L_ii (warp 0, kCvNll)
 
         // ---------------- blocked left-looking Cholesky with bordered y row ----------------
         for (int jb = 0; jb < nblk && !failed; ++jb) {
@@ -368,6 +370,11 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         failed = true;
                         break;
                     }
+                    if ((a.flags & kCvNll) && warp == 0) {  // log det of this diagonal block
+                        double l = 0.0;
+                        for (int q = lane; q < jw; q += 32) l += log(dg[q]);
+                        logdet += warp_sum(l);
+                    }
                     // L_jj -> the factor (lower triangle; the diagonal from the pivots)
                     for (int e = tid; e < jw * jw; e += NT) {
                         const int rr = e / jw, cc = e % jw;
@@ -446,9 +453,43 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 
         if (failed) {
             if (tid == 0) {
-                a.subset_loss[(int64_t)s * a.C + c] = __longlong_as_double(0x7ff8000000000000ll);
-                a.fail[(int64_t)s * a.C + c] = 1;
+                const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+                if (a.flags & kCvPredict) a.subset_loss[oi] = qnan;
+                if (a.flags & kCvNll) a.subset_nll[oi] = qnan;
+                a.fail[oi] = 1;
             }
+            continue;
+        }
+
+        // ---------------- -2 log-likelihood (Eq.2) from the same factor ----------
+        // sigma2 Sigma + tau I = sigma2 (Sigma + lambda I) = sigma2 L L^T, so
+        //   log det = k log sigma2 + 2 sum log L_ii,  y^T (.)^{-1} y = ||z||^2 / sigma2,
+        // with z = L^{-1} y_T the bordered row k of the factor.
+        if (a.flags & kCvNll) {
+            double zz = 0.0;
+            for (int cc = tid; cc < k; cc += NT) {
+                const double zc = __ldcg(L + lidx(ld, k, cc));
+                zz += zc * zc;
+            }
+            zz = warp_sum(zz);
+            if (lane == 0) red[warp] = zz;
+            __syncthreads();
+            if (tid == 0) {
+                double q = 0.0;
+                for (int w = 0; w < NWARP; ++w) q += red[w];
+                const double kd = (double)k;
+                a.subset_nll[oi] = kd * log(2.0 * 3.14159265358979323846) + kd * log(sigma2) +
+                                   2.0 * logdet + q / sigma2;
+            }
+            __syncthreads();
+        }
+        if (!(a.flags & kCvPredict) || m == 0) {
+            if (tid == 0) {
+                if (a.flags & kCvPredict) a.subset_loss[oi] = 0.0;  // R10: no targets
+                a.fail[oi] = 0;
+            }
+            fence_proxy_async();
+            __syncthreads();
             continue;
         }
 
@@ -518,6 +559,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 sum += exp(sqrt(dx * dx + dy * dy) * ninv) * alpha[j];
             }
             sum = warp_sum(sum);
+            if (a.yhat && lane == 0) a.yhat[voff + v] = sum;
             const double e = sum - __ldg(vv + v);
             part += e * e;
         }
@@ -527,29 +569,32 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         if (tid == 0) {
             double l = 0.0;
             for (int w = 0; w < NWARP; ++w) l += red[w];
-            a.subset_loss[(int64_t)s * a.C + c] = l;
-            a.fail[(int64_t)s * a.C + c] = 0;
+            a.subset_loss[oi] = l;
+            a.fail[oi] = 0;
         }
     }
 }
 
-// loss[c] = sum_s subset_loss[s, c] in ascending s (Alg.1 line 9); status[c] = the
-// smallest failing subset or -1.  One thread per config: a fixed, deterministic order.
-__global__ void reduce_kernel(const double *subset_loss, const uint8_t *fail, int64_t N, int32_t C,
-                              double *loss, int32_t *status) {
+// out[c] = sum_s vals[s, c] in ascending s (Alg.1 line 9) over the subsets the
+// mask admits (mask_off[s+1] > mask_off[s], i.e. subsets with targets; all when null);
+// status[c] = the smallest failing admitted subset or -1.  One thread per config: a fixed,
+// deterministic order.
+__global__ void reduce_kernel(const double *vals, const uint8_t *fail, const int64_t *mask_off, int64_t N,
+                              int32_t C, double *out, int32_t *status) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C) return;
     double acc = 0.0;
     int64_t st = -1;
     for (int64_t s = 0; s < N; ++s) {
+        if (mask_off && mask_off[s + 1] == mask_off[s]) continue;
         if (fail[s * C + c]) {
             if (st < 0) st = s;
         } else {
-            acc += subset_loss[s * C + c];
+            acc += vals[s * C + c];
         }
     }
-    loss[c] = st >= 0 ? __longlong_as_double(0x7ff8000000000000ll) : acc;
-    status[c] = (int32_t)st;
+    out[c] = st >= 0 ? __longlong_as_double(0x7ff8000000000000ll) : acc;
+    if (status) status[c] = (int32_t)st;
 }
 
 }  // namespace
@@ -581,9 +626,9 @@ cudaError_t launch_cv_kernel(const CvArgs &a, int grid, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_reduce(const double *subset_loss, const uint8_t *fail, int64_t N, int32_t C,
-                          double *loss, int32_t *status, cudaStream_t st) {
-    reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(subset_loss, fail, N, C, loss, status);
+cudaError_t launch_reduce(const double *vals, const uint8_t *fail, const int64_t *mask_off, int64_t N,
+                          int32_t C, double *out, int32_t *status, cudaStream_t st) {
+    reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(vals, fail, mask_off, N, C, out, status);
     return cudaGetLastError();
 }
 

@@ -67,14 +67,15 @@ __global__ void validate_kernel(int64_t n, const double *x, const double *y, con
 }
 
 __global__ void count_kernel(int64_t n, const double *x, const double *y, const uint8_t *role,
-                             Axis ax, Axis ay, unsigned int *train_cnt, unsigned int *val_cnt) {
+                             Axis ax, Axis ay, unsigned int *train_cnt, unsigned int *val_cnt,
+                             unsigned int *test_cnt) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         const uint8_t r = role[p];
         const double px = x[p], py = y[p];
-        if (r == 1) {
+        if (r == 1 || r == 2) {
             const int ix = core_index(px, ax.e, ax.K), iy = core_index(py, ay.e, ay.K);
-            atomicAdd(val_cnt + (int64_t)iy * ax.K + ix, 1u);
+            atomicAdd((r == 1 ? val_cnt : test_cnt) + (int64_t)iy * ax.K + ix, 1u);
         } else if (r == 0) {
             const int2 rx = dilated_range(px, ax), ry = dilated_range(py, ay);
             for (int iy = ry.x; iy <= ry.y; ++iy)
@@ -86,8 +87,9 @@ __global__ void count_kernel(int64_t n, const double *x, const double *y, const 
 
 __global__ void scatter_kernel(int64_t n, const double *x, const double *y, const uint8_t *role,
                                Axis ax, Axis ay, const int64_t *train_off, const int64_t *val_off,
-                               unsigned int *train_cur, unsigned int *val_cur, int32_t *train_idx,
-                               int32_t *val_idx) {
+                               const int64_t *test_off, unsigned int *train_cur, unsigned int *val_cur,
+                               unsigned int *test_cur, int32_t *train_idx, int32_t *val_idx,
+                               int32_t *test_idx) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         const uint8_t r = role[p];
@@ -96,6 +98,10 @@ __global__ void scatter_kernel(int64_t n, const double *x, const double *y, cons
             const int ix = core_index(px, ax.e, ax.K), iy = core_index(py, ay.e, ay.K);
             const int64_t s = (int64_t)iy * ax.K + ix;
             val_idx[val_off[s] + atomicAdd(val_cur + s, 1u)] = (int32_t)p;
+        } else if (r == 2) {  // test points: core tile only, targets of pgpcv_predict
+            const int ix = core_index(px, ax.e, ax.K), iy = core_index(py, ay.e, ay.K);
+            const int64_t s = (int64_t)iy * ax.K + ix;
+            test_idx[test_off[s] + atomicAdd(test_cur + s, 1u)] = (int32_t)p;
         } else if (r == 0) {
             const int2 rx = dilated_range(px, ax), ry = dilated_range(py, ay);
             for (int iy = ry.x; iy <= ry.y; ++iy)
@@ -228,9 +234,9 @@ cudaError_t launch_validate(int64_t n, const double *x, const double *y, const d
 
 cudaError_t launch_count(int64_t n, const double *x, const double *y, const uint8_t *role,
                          Axis ax, Axis ay, unsigned int *train_cnt, unsigned int *val_cnt,
-                         cudaStream_t st) {
+                         unsigned int *test_cnt, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    count_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, ax, ay, train_cnt, val_cnt);
+    count_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, ax, ay, train_cnt, val_cnt, test_cnt);
     return cudaGetLastError();
 }
 
@@ -241,11 +247,13 @@ cudaError_t launch_scan(const unsigned int *cnt, int64_t N, int64_t *off, cudaSt
 
 cudaError_t launch_scatter(int64_t n, const double *x, const double *y, const uint8_t *role,
                            Axis ax, Axis ay, const int64_t *train_off, const int64_t *val_off,
-                           unsigned int *train_cur, unsigned int *val_cur, int32_t *train_idx,
-                           int32_t *val_idx, cudaStream_t st) {
+                           const int64_t *test_off, unsigned int *train_cur, unsigned int *val_cur,
+                           unsigned int *test_cur, int32_t *train_idx, int32_t *val_idx,
+                           int32_t *test_idx, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, ax, ay, train_off, val_off,
-                                                train_cur, val_cur, train_idx, val_idx);
+    scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, ax, ay, train_off, val_off, test_off,
+                                                train_cur, val_cur, test_cur, train_idx, val_idx,
+                                                test_idx);
     return cudaGetLastError();
 }
 

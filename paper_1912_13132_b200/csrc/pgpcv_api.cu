@@ -95,12 +95,6 @@ __global__ void status_encode(int32_t *st, int32_t C, int32_t sentinel) {
     if (c < C && st[c] == sentinel) st[c] = (sentinel == -1) ? 0x7fffffff : -1;
 }
 
-double subset_flops(double k, double m) {
-    // Cholesky k^3/3 + k^2/2 + k/6, two triangular solves 2k^2,
-    // prediction 2mk, residual and square 3m.  exp/sqrt are not counted.
-    return k * k * k / 3.0 + k * k / 2.0 + k / 6.0 + 2.0 * k * k + 2.0 * m * k + 3.0 * m;
-}
-
 // R4: e_i = a + i*w (separate multiply and add), e_K = b; bounds e_i - delta, e_{i+1} + delta.
 bool axis_bounds(double a, double b, int K, double delta, std::vector<double> &e,
                  std::vector<double> &lo, std::vector<double> &hi) {
@@ -142,11 +136,11 @@ struct pgpcv_ctx {
     DevBuf<double> bounds;  // ex, lox, hix, ey, loy, hiy
     DevBuf<unsigned int> cnt, cur;
     DevBuf<unsigned long long> stats;
-    DevBuf<int64_t> train_off, val_off;
-    DevBuf<int32_t> train_idx, val_idx;
+    DevBuf<int64_t> train_off, val_off, test_off;
+    DevBuf<int32_t> train_idx, val_idx, test_idx;
     DevBuf<uint32_t> bitmap;
-    DevBuf<double> tx, ty, tv, vx, vy, vv;
-    std::vector<int64_t> h_train_off, h_val_off;
+    DevBuf<double> tx, ty, tv, vx, vy, vv, gx, gy, gv;  // g*: staged test points
+    std::vector<int64_t> h_train_off, h_val_off, h_test_off;
     pgpcv_partition_info info{};
 
     // sharding
@@ -160,9 +154,17 @@ struct pgpcv_ctx {
     DevBuf<double> params;
     DevBuf<int2> items;
     DevBuf<unsigned int> counter;
-    DevBuf<double> subset_loss, loss;
+    DevBuf<double> subset_loss, subset_nll, sums;  // sums: [loss C | nll C]
     DevBuf<uint8_t> fail;
-    DevBuf<int32_t> status;
+    DevBuf<int32_t> status;                        // [loss C | nll C]
+    // pgpcv_predict
+    DevBuf<double> p_sub, p_yhat, p_sum;
+    DevBuf<uint8_t> p_fail;
+    DevBuf<int32_t> p_status;
+    // pgpcv_select: the last evaluation's device-resident per-subset losses
+    int32_t sel_C = 0;
+    DevBuf<double> sel_rmspe, sel_local;
+    DevBuf<int32_t> sel_best, sel_wins;
     int blocks_per_sm = 0;
     pgpcv_timing timing{};
     bool has_timing = false;
@@ -243,42 +245,52 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     ctx->kx = kx;
     ctx->ky = ky;
     // K1 count, K2 scan
-    CK(ctx->cnt.ensure(2 * N), "alloc counts");
-    CK(ctx->cur.ensure(2 * N), "alloc cursors");
+    CK(ctx->cnt.ensure(3 * N), "alloc counts");
+    CK(ctx->cur.ensure(3 * N), "alloc cursors");
     CK(ctx->train_off.ensure(N + 1), "alloc offsets");
     CK(ctx->val_off.ensure(N + 1), "alloc offsets");
-    CK(cudaMemsetAsync(ctx->cnt.p, 0, sizeof(unsigned) * 2 * N, st), "memset");
-    CK(launch_count(n, x, y, role, ax, ay, ctx->cnt.p, ctx->cnt.p + N, st), "count kernel");
+    CK(ctx->test_off.ensure(N + 1), "alloc offsets");
+    CK(cudaMemsetAsync(ctx->cnt.p, 0, sizeof(unsigned) * 3 * N, st), "memset");
+    CK(launch_count(n, x, y, role, ax, ay, ctx->cnt.p, ctx->cnt.p + N, ctx->cnt.p + 2 * N, st),
+       "count kernel");
     CK(launch_scan(ctx->cnt.p, N, ctx->train_off.p, st), "scan kernel");
     CK(launch_scan(ctx->cnt.p + N, N, ctx->val_off.p, st), "scan kernel");
+    CK(launch_scan(ctx->cnt.p + 2 * N, N, ctx->test_off.p, st), "scan kernel");
     ctx->h_train_off.resize(N + 1);
     ctx->h_val_off.resize(N + 1);
+    ctx->h_test_off.resize(N + 1);
     CK(cudaMemcpyAsync(ctx->h_train_off.data(), ctx->train_off.p, sizeof(int64_t) * (N + 1),
                        cudaMemcpyDeviceToHost, st), "copy offsets");
     CK(cudaMemcpyAsync(ctx->h_val_off.data(), ctx->val_off.p, sizeof(int64_t) * (N + 1),
                        cudaMemcpyDeviceToHost, st), "copy offsets");
+    CK(cudaMemcpyAsync(ctx->h_test_off.data(), ctx->test_off.p, sizeof(int64_t) * (N + 1),
+                       cudaMemcpyDeviceToHost, st), "copy offsets");
     CK(cudaStreamSynchronize(st), "scan");
-    const int64_t sum_k = ctx->h_train_off[N], sum_m = ctx->h_val_off[N];
+    const int64_t sum_k = ctx->h_train_off[N], sum_m = ctx->h_val_off[N], sum_g = ctx->h_test_off[N];
     if (sum_k >= (int64_t)1 << 31 || sum_m >= (int64_t)1 << 31)
         return ctx->fail_with(PGPCV_EINVAL, "more than 2^31 memberships");
     // K3 scatter + per-segment sort into ascending index order
     CK(ctx->train_idx.ensure(sum_k), "alloc train_idx");
     CK(ctx->val_idx.ensure(sum_m), "alloc val_idx");
-    CK(cudaMemsetAsync(ctx->cur.p, 0, sizeof(unsigned) * 2 * N, st), "memset");
-    CK(launch_scatter(n, x, y, role, ax, ay, ctx->train_off.p, ctx->val_off.p, ctx->cur.p,
-                      ctx->cur.p + N, ctx->train_idx.p, ctx->val_idx.p, st), "scatter kernel");
-    int64_t max_k = 0, max_m = 0, empty = 0;
+    CK(ctx->test_idx.ensure(sum_g), "alloc test_idx");
+    CK(cudaMemsetAsync(ctx->cur.p, 0, sizeof(unsigned) * 3 * N, st), "memset");
+    CK(launch_scatter(n, x, y, role, ax, ay, ctx->train_off.p, ctx->val_off.p, ctx->test_off.p,
+                      ctx->cur.p, ctx->cur.p + N, ctx->cur.p + 2 * N, ctx->train_idx.p,
+                      ctx->val_idx.p, ctx->test_idx.p, st), "scatter kernel");
+    int64_t max_k = 0, max_m = 0, max_g = 0, empty = 0;
     for (int64_t s = 0; s < N; ++s) {
         max_k = std::max(max_k, ctx->h_train_off[s + 1] - ctx->h_train_off[s]);
         const int64_t m = ctx->h_val_off[s + 1] - ctx->h_val_off[s];
         max_m = std::max(max_m, m);
+        max_g = std::max(max_g, ctx->h_test_off[s + 1] - ctx->h_test_off[s]);
         empty += m == 0;
     }
     CK(launch_segsort_small(ctx->train_idx.p, ctx->train_off.p, N, max_k, st), "segsort");
     CK(launch_segsort_small(ctx->val_idx.p, ctx->val_off.p, N, max_m, st), "segsort");
-    for (int which = 0; which < 2; ++which) {
-        const std::vector<int64_t> &off = which ? ctx->h_val_off : ctx->h_train_off;
-        int32_t *idx = which ? ctx->val_idx.p : ctx->train_idx.p;
+    CK(launch_segsort_small(ctx->test_idx.p, ctx->test_off.p, N, max_g, st), "segsort");
+    for (int which = 0; which < 3; ++which) {
+        const std::vector<int64_t> &off = which == 2 ? ctx->h_test_off : which ? ctx->h_val_off : ctx->h_train_off;
+        int32_t *idx = which == 2 ? ctx->test_idx.p : which ? ctx->val_idx.p : ctx->train_idx.p;
         for (int64_t s = 0; s < N; ++s) {
             const int64_t len = off[s + 1] - off[s];
             if (len > kSmallSortMax) {
@@ -294,8 +306,12 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     CK(ctx->vx.ensure(sum_m), "alloc");
     CK(ctx->vy.ensure(sum_m), "alloc");
     CK(ctx->vv.ensure(sum_m), "alloc");
+    CK(ctx->gx.ensure(sum_g), "alloc");
+    CK(ctx->gy.ensure(sum_g), "alloc");
+    CK(ctx->gv.ensure(sum_g), "alloc");
     CK(launch_gather(sum_k, ctx->train_idx.p, x, y, v, ctx->tx.p, ctx->ty.p, ctx->tv.p, st), "gather");
     CK(launch_gather(sum_m, ctx->val_idx.p, x, y, v, ctx->vx.p, ctx->vy.p, ctx->vv.p, st), "gather");
+    CK(launch_gather(sum_g, ctx->test_idx.p, x, y, v, ctx->gx.p, ctx->gy.p, ctx->gv.p, st), "gather");
     CK(cudaStreamSynchronize(st), "partition");
 
     pgpcv_partition_info &info = ctx->info;
@@ -307,8 +323,11 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     info.n_empty_val = empty;
     info.n_train = (int64_t)hstats[1];
     info.n_val = (int64_t)hstats[2];
+    info.n_test = sum_g;
+    info.max_test = max_g;
     ctx->has_partition = true;
     ctx->cv_done = false;
+    ctx->sel_C = 0;
     assign_owned(ctx);
     if (info_out) *info_out = info;
     return PGPCV_OK;
@@ -498,62 +517,61 @@ int pgpcv_shard(pgpcv_ctx *ctx, int rank, int world, const void *nccl_unique_id)
     return PGPCV_OK;
 }
 
-int pgpcv_cv_loss(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, double *loss,
-                  double *subset_loss, int32_t *status) {
-    if (!ctx) return PGPCV_EINVAL;
-    if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "pgpcv_cv_loss needs a partition");
-    if (n_params < 1 || !params || !loss) return ctx->fail_with(PGPCV_EINVAL, "bad params/loss");
+}  // extern "C"
+
+namespace {
+
+int check_params(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params) {
+    if (n_params < 1 || !params) return ctx->fail_with(PGPCV_EINVAL, "need n_params >= 1 configurations");
     for (int c = 0; c < n_params; ++c) {
         const pgpcv_param &p = params[c];
         if (!(p.range > 0) || !(p.sigma2 > 0) || !(p.nugget >= 0) || !std::isfinite(p.range) ||
             !std::isfinite(p.sigma2) || !std::isfinite(p.nugget))
             return ctx->fail_with(PGPCV_EINVAL, "config %d: need range > 0, sigma2 > 0, nugget >= 0", c);
     }
-    if (ctx->info.sum_m == 0) return ctx->fail_with(PGPCV_EEMPTY, "no subset has validation data");
-    cudaSetDevice(ctx->device);
-    cudaStream_t st = ctx->stream;
-    const int64_t N = ctx->N;
-    const int32_t C = n_params;
+    return PGPCV_OK;
+}
 
-    // work items: owned subsets with validation data, descending k (LPT), all configs
-    std::vector<int32_t> subs;
-    for (int64_t s = 0; s < N; ++s)
-        if (ctx->owned[s] && ctx->h_val_off[s + 1] > ctx->h_val_off[s]) subs.push_back((int32_t)s);
-    std::stable_sort(subs.begin(), subs.end(), [&](int32_t a, int32_t b) {
-        return ctx->h_train_off[a + 1] - ctx->h_train_off[a] > ctx->h_train_off[b + 1] - ctx->h_train_off[b];
+// One launch of the batched CV kernel over `items` (subset, config) in LPT order, with the
+// factor workspace sized for the largest subset; records the launch's CUDA-event time on
+// ctx->ev[1..2].  Outputs are device arrays of stride out_C (see CvArgs).
+struct CvLaunch {
+    int32_t flags = 0;
+    const pgpcv_param *params = nullptr;
+    int32_t C = 0;
+    std::vector<int2> items;
+    int32_t out_C = 1;
+    const int64_t *tgt_off = nullptr;
+    const double *gx = nullptr, *gy = nullptr, *gv = nullptr;
+    double *subset_loss = nullptr, *subset_nll = nullptr, *yhat = nullptr;
+    uint8_t *fail = nullptr;
+    double flops = 0;
+    int slots = 0;
+};
+
+int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
+    cudaStream_t st = ctx->stream;
+    // LPT: descending k (stable, so ties keep ascending subset / config order)
+    std::stable_sort(L.items.begin(), L.items.end(), [&](const int2 &a, const int2 &b) {
+        return ctx->h_train_off[a.x + 1] - ctx->h_train_off[a.x] > ctx->h_train_off[b.x + 1] - ctx->h_train_off[b.x];
     });
     int64_t kmax = 0;
-    double flops = 0;
-    std::vector<int2> items;
-    items.reserve(subs.size() * C);
-    for (int32_t s : subs) {
-        const int64_t k = ctx->h_train_off[s + 1] - ctx->h_train_off[s];
-        const int64_t m = ctx->h_val_off[s + 1] - ctx->h_val_off[s];
-        kmax = std::max(kmax, k);
-        for (int32_t c = 0; c < C; ++c) items.push_back(make_int2(s, c));
-        flops += C * subset_flops((double)k, (double)m);
-    }
+    for (const int2 &it : L.items) kmax = std::max(kmax, ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]);
     if (kmax > cv_kernel_max_k())
-        return ctx->fail_with(PGPCV_EINVAL, "a subset has %lld training points (max %d)",
-                              (long long)kmax, cv_kernel_max_k());
-    const int64_t n_items = (int64_t)items.size();
+        return ctx->fail_with(PGPCV_EINVAL, "a subset has %lld training points (max %d)", (long long)kmax,
+                              cv_kernel_max_k());
+    const int64_t n_items = (int64_t)L.items.size();
     if (n_items >= ((int64_t)1 << 31)) return ctx->fail_with(PGPCV_EINVAL, "too many work items");
-
-    std::vector<double> hp(3 * (size_t)C);
-    for (int c = 0; c < C; ++c) {
-        hp[3 * c] = params[c].range;
-        hp[3 * c + 1] = params[c].sigma2;
-        hp[3 * c + 2] = params[c].nugget;
+    std::vector<double> hp(3 * (size_t)L.C);
+    for (int c = 0; c < L.C; ++c) {
+        hp[3 * c] = L.params[c].range;
+        hp[3 * c + 1] = L.params[c].sigma2;
+        hp[3 * c + 2] = L.params[c].nugget;
     }
-    CK(ctx->params.ensure(3 * (size_t)C), "alloc params");
+    CK(ctx->params.ensure(3 * (size_t)L.C), "alloc params");
     CK(ctx->items.ensure(std::max<int64_t>(n_items, 1)), "alloc items");
     CK(ctx->counter.ensure(1), "alloc counter");
-    CK(ctx->subset_loss.ensure((size_t)N * C), "alloc subset_loss");
-    CK(ctx->fail.ensure((size_t)N * C), "alloc fail");
-    CK(ctx->loss.ensure(C), "alloc loss");
-    CK(ctx->status.ensure(C), "alloc status");
-
-    // factor workspace: one column-major (k+1) x k factor per resident CTA
+    // factor workspace: one (k+1) x k factor per resident CTA
     int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_items, 1));
     if (const char *env = getenv("PGPCV_MAX_SLOTS")) {  // diagnostics: cap resident CTAs
         const int cap = atoi(env);
@@ -566,95 +584,314 @@ int pgpcv_cv_loss(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, d
         if (slots == 1) return ctx->cuda_fail(e, "alloc factor workspace");
         slots = std::max(1, slots / 2);
     }
-
-    CK(cudaEventRecord(ctx->ev[0], st), "event");
+    L.slots = slots;
     CK(cudaMemcpyAsync(ctx->params.p, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, st),
        "copy params");
     if (n_items)
-        CK(cudaMemcpyAsync(ctx->items.p, items.data(), sizeof(int2) * n_items, cudaMemcpyHostToDevice, st),
+        CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_items, cudaMemcpyHostToDevice, st),
            "copy items");
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned), st), "memset");
-    CK(cudaMemsetAsync(ctx->subset_loss.p, 0, sizeof(double) * N * C, st), "memset");
-    CK(cudaMemsetAsync(ctx->fail.p, 0, (size_t)N * C, st), "memset");
-    int launches = 0;
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     if (n_items) {
         CvArgs a;
         a.train_off = ctx->train_off.p;
-        a.val_off = ctx->val_off.p;
+        a.val_off = L.tgt_off;
         a.tx = ctx->tx.p;
         a.ty = ctx->ty.p;
         a.tv = ctx->tv.p;
-        a.vx = ctx->vx.p;
-        a.vy = ctx->vy.p;
-        a.vv = ctx->vv.p;
+        a.vx = L.gx;
+        a.vy = L.gy;
+        a.vv = L.gv;
         a.params = ctx->params.p;
-        a.C = C;
+        a.C = L.C;
         a.items = ctx->items.p;
         a.n_items = (int32_t)n_items;
         a.counter = ctx->counter.p;
         a.work = ctx->work.p;
         a.slot_stride = slot_stride;
-        a.subset_loss = ctx->subset_loss.p;
-        a.fail = ctx->fail.p;
+        a.out_C = L.out_C;
+        a.flags = L.flags;
+        a.subset_loss = L.subset_loss;
+        a.subset_nll = L.subset_nll;
+        a.yhat = L.yhat;
+        a.fail = L.fail;
         CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
-        ++launches;
     }
     CK(cudaEventRecord(ctx->ev[2], st), "event");
+    return PGPCV_OK;
+}
 
-    NcclApi &api = nccl();
-    const bool multi = ctx->world > 1;
-    if (multi && subset_loss) {
-        // each (s, c) entry has exactly one owner (others hold 0): the sum is exact, and the
-        // global reduction below then runs on identical arrays on every rank.
-        ncclResult_t r = api.allReduce(ctx->subset_loss.p, ctx->subset_loss.p, (size_t)N * C,
-                                       ncclFloat64, ncclSum, ctx->comm, st);
-        if (r == ncclSuccess)
-            r = api.allReduce(ctx->fail.p, ctx->fail.p, (size_t)N * C, ncclUint8, ncclSum, ctx->comm, st);
-        if (r != ncclSuccess) return ctx->fail_with(PGPCV_ENCCL, "ncclAllReduce: %s", api.getErrorString(r));
-    }
-    CK(launch_reduce(ctx->subset_loss.p, ctx->fail.p, N, C, ctx->loss.p, ctx->status.p, st), "reduce");
-    ++launches;
-    if (multi && !subset_loss) {
-        // Alg.1 line 9 across GPUs: one all-reduce of the per-configuration loss vector.
-        ncclResult_t r = api.allReduce(ctx->loss.p, ctx->loss.p, C, ncclFloat64, ncclSum, ctx->comm, st);
-        status_encode<<<(C + 127) / 128, 128, 0, st>>>(ctx->status.p, C, -1);
-        ++launches;
-        if (r == ncclSuccess)
-            r = api.allReduce(ctx->status.p, ctx->status.p, C, ncclInt32, ncclMin, ctx->comm, st);
-        status_encode<<<(C + 127) / 128, 128, 0, st>>>(ctx->status.p, C, 0x7fffffff);
-        ++launches;
-        if (r != ncclSuccess) return ctx->fail_with(PGPCV_ENCCL, "ncclAllReduce: %s", api.getErrorString(r));
-    }
-    std::vector<int32_t> hstatus(C);
-    CK(cudaMemcpyAsync(loss, ctx->loss.p, sizeof(double) * C, cudaMemcpyDeviceToHost, st), "copy loss");
-    CK(cudaMemcpyAsync(hstatus.data(), ctx->status.p, sizeof(int32_t) * C, cudaMemcpyDeviceToHost, st),
-       "copy status");
-    if (subset_loss)
-        CK(cudaMemcpyAsync(subset_loss, ctx->subset_loss.p, sizeof(double) * N * C, cudaMemcpyDeviceToHost, st),
-           "copy subset_loss");
-    CK(cudaEventRecord(ctx->ev[3], st), "event");
-    CK(cudaStreamSynchronize(st), "cv_loss");
-    CK(cudaGetLastError(), "cv_loss");
-    ctx->cv_done = true;
-
+void record_timing(pgpcv_ctx *ctx, const CvLaunch &L, int launches) {
     float kms = 0, tms = 0;
     cudaEventElapsedTime(&kms, ctx->ev[1], ctx->ev[2]);
     cudaEventElapsedTime(&tms, ctx->ev[0], ctx->ev[3]);
     ctx->timing.kernel_ms = kms;
     ctx->timing.total_ms = tms;
-    ctx->timing.flops = flops;
-    ctx->timing.n_evals = n_items;
+    ctx->timing.flops = L.flops;
+    ctx->timing.n_evals = (int64_t)L.items.size();
     ctx->timing.launches = launches;
-    ctx->timing.n_slots = slots;
+    ctx->timing.n_slots = L.slots;
     ctx->has_timing = true;
+}
+
+int nccl_sum(pgpcv_ctx *ctx, void *buf, size_t count, ncclDataType_t t) {
+    NcclApi &api = nccl();
+    ncclResult_t r = api.allReduce(buf, buf, count, t, ncclSum, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return ctx->fail_with(PGPCV_ENCCL, "ncclAllReduce: %s", api.getErrorString(r));
+    return PGPCV_OK;
+}
+
+int first_fail(int32_t a, int32_t b) { return a < 0 ? b : (b < 0 ? a : std::min(a, b)); }
+
+}  // namespace
+
+extern "C" {
+
+int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, const pgpcv_outputs *out) {
+    if (!ctx) return PGPCV_EINVAL;
+    if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "evaluation needs a partition");
+    if (!out) return ctx->fail_with(PGPCV_EINVAL, "NULL outputs");
+    int rc = check_params(ctx, params, n_params);
+    if (rc) return rc;
+    const bool want_cv = out->loss || out->subset_loss;
+    const bool want_nll = out->nll || out->subset_nll;
+    if (!want_cv && !want_nll) return ctx->fail_with(PGPCV_EINVAL, "no output requested");
+    if (want_cv && ctx->info.sum_m == 0) return ctx->fail_with(PGPCV_EEMPTY, "no subset has validation data");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t N = ctx->N;
+    const int32_t C = n_params;
+    ctx->sel_C = 0;
+
+    CvLaunch L;
+    L.flags = (want_cv ? kCvPredict : 0) | (want_nll ? kCvNll : 0);
+    L.params = params;
+    L.C = C;
+    L.out_C = C;
+    L.tgt_off = ctx->val_off.p;
+    L.gx = ctx->vx.p;
+    L.gy = ctx->vy.p;
+    L.gv = ctx->vv.p;
+    // work items: owned subsets with validation data (all owned subsets when the likelihood
+    // is requested: it needs no targets), every config
+    for (int64_t s = 0; s < N; ++s) {
+        const int64_t k = ctx->h_train_off[s + 1] - ctx->h_train_off[s];
+        const int64_t m = ctx->h_val_off[s + 1] - ctx->h_val_off[s];
+        if (!ctx->owned[s] || (m == 0 && !want_nll)) continue;
+        for (int32_t c = 0; c < C; ++c) L.items.push_back(make_int2((int)s, c));
+        // the Cholesky and forward solve count for every item; the backward
+        // solve, prediction and residuals only where validation data are predicted.
+        const double kd = (double)k, md = (double)m;
+        double f = kd * kd * kd / 3.0 + kd * kd / 2.0 + kd / 6.0 + kd * kd;
+        if (want_cv && m > 0) f += kd * kd + 2.0 * md * kd + 3.0 * md;
+        L.flops += C * f;
+    }
+    CK(ctx->subset_loss.ensure((size_t)N * C), "alloc subset_loss");
+    CK(ctx->subset_nll.ensure((size_t)N * C), "alloc subset_nll");
+    CK(ctx->fail.ensure((size_t)N * C), "alloc fail");
+    CK(ctx->sums.ensure(2 * (size_t)C), "alloc sums");
+    CK(ctx->status.ensure(2 * (size_t)C), "alloc status");
+    L.subset_loss = ctx->subset_loss.p;
+    L.subset_nll = ctx->subset_nll.p;
+    L.fail = ctx->fail.p;
+
+    CK(cudaEventRecord(ctx->ev[0], st), "event");
+    CK(cudaMemsetAsync(ctx->subset_loss.p, 0, sizeof(double) * N * C, st), "memset");
+    CK(cudaMemsetAsync(ctx->subset_nll.p, 0, sizeof(double) * N * C, st), "memset");
+    CK(cudaMemsetAsync(ctx->fail.p, 0, (size_t)N * C, st), "memset");
+    if ((rc = run_cv(ctx, L))) return rc;
+    int launches = L.items.empty() ? 0 : 1;
+
+    const bool multi = ctx->world > 1;
+    const bool gather = multi && (out->subset_loss || out->subset_nll);
+    if (gather) {
+        // each (s, c) entry has exactly one owner (others hold 0): the sums are exact, and
+        // the global reductions below then run on identical arrays on every rank.
+        if (want_cv && (rc = nccl_sum(ctx, ctx->subset_loss.p, (size_t)N * C, ncclFloat64))) return rc;
+        if (want_nll && (rc = nccl_sum(ctx, ctx->subset_nll.p, (size_t)N * C, ncclFloat64))) return rc;
+        if ((rc = nccl_sum(ctx, ctx->fail.p, (size_t)N * C, ncclUint8))) return rc;
+    }
+    double *d_loss = ctx->sums.p, *d_nll = ctx->sums.p + C;
+    int32_t *d_st_loss = ctx->status.p, *d_st_nll = ctx->status.p + C;
+    if (want_cv) {
+        CK(launch_reduce(ctx->subset_loss.p, ctx->fail.p, ctx->val_off.p, N, C, d_loss, d_st_loss, st), "reduce");
+        ++launches;
+    }
+    if (want_nll) {
+        CK(launch_reduce(ctx->subset_nll.p, ctx->fail.p, nullptr, N, C, d_nll, d_st_nll, st), "reduce");
+        ++launches;
+    }
+    if (multi && !gather) {
+        // Alg.1 line 9 across GPUs: one all-reduce of the per-configuration [loss | nll]
+        // vector, and a MIN all-reduce of the statuses.
+        if (!want_cv) CK(cudaMemsetAsync(d_loss, 0, sizeof(double) * C, st), "memset");
+        if (!want_nll) CK(cudaMemsetAsync(d_nll, 0, sizeof(double) * C, st), "memset");
+        if (!want_cv) CK(cudaMemsetAsync(d_st_loss, 0xff, sizeof(int32_t) * C, st), "memset");
+        if (!want_nll) CK(cudaMemsetAsync(d_st_nll, 0xff, sizeof(int32_t) * C, st), "memset");
+        if ((rc = nccl_sum(ctx, ctx->sums.p, 2 * (size_t)C, ncclFloat64))) return rc;
+        status_encode<<<(2 * C + 127) / 128, 128, 0, st>>>(ctx->status.p, 2 * C, -1);
+        NcclApi &api = nccl();
+        ncclResult_t r = api.allReduce(ctx->status.p, ctx->status.p, 2 * (size_t)C, ncclInt32, ncclMin, ctx->comm, st);
+        status_encode<<<(2 * C + 127) / 128, 128, 0, st>>>(ctx->status.p, 2 * C, 0x7fffffff);
+        launches += 2;
+        if (r != ncclSuccess) return ctx->fail_with(PGPCV_ENCCL, "ncclAllReduce: %s", api.getErrorString(r));
+    }
+    std::vector<double> hsums(2 * (size_t)C);
+    std::vector<int32_t> hstatus(2 * (size_t)C, -1);
+    CK(cudaMemcpyAsync(hsums.data(), ctx->sums.p, sizeof(double) * 2 * C, cudaMemcpyDeviceToHost, st), "copy sums");
+    CK(cudaMemcpyAsync(hstatus.data(), ctx->status.p, sizeof(int32_t) * 2 * C, cudaMemcpyDeviceToHost, st),
+       "copy status");
+    if (out->subset_loss)
+        CK(cudaMemcpyAsync(out->subset_loss, ctx->subset_loss.p, sizeof(double) * N * C, cudaMemcpyDeviceToHost, st),
+           "copy subset_loss");
+    if (out->subset_nll)
+        CK(cudaMemcpyAsync(out->subset_nll, ctx->subset_nll.p, sizeof(double) * N * C, cudaMemcpyDeviceToHost, st),
+           "copy subset_nll");
+    CK(cudaEventRecord(ctx->ev[3], st), "event");
+    CK(cudaStreamSynchronize(st), "evaluate");
+    CK(cudaGetLastError(), "evaluate");
+    ctx->cv_done = true;
+    record_timing(ctx, L, launches);
+    if (want_cv && (!multi || gather)) ctx->sel_C = C;  // every subset's loss is on this device
 
     bool any_fail = false;
     for (int c = 0; c < C; ++c) {
-        if (status) status[c] = hstatus[c];
-        any_fail |= hstatus[c] >= 0;
+        const int32_t sl = want_cv ? hstatus[c] : -1, sn = want_nll ? hstatus[C + c] : -1;
+        if (out->loss) out->loss[c] = hsums[c];
+        if (out->nll) out->nll[c] = hsums[C + c];
+        const int32_t f = first_fail(sl, sn);
+        if (out->status) out->status[c] = f;
+        any_fail |= f >= 0;
     }
     if (any_fail) return ctx->fail_with(PGPCV_ENUMERIC, "some configuration was not positive definite");
+    return PGPCV_OK;
+}
+
+int pgpcv_cv_loss(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, double *loss,
+                  double *subset_loss, int32_t *status) {
+    if (!ctx) return PGPCV_EINVAL;
+    if (!loss) return ctx->fail_with(PGPCV_EINVAL, "NULL loss");
+    pgpcv_outputs o{};
+    o.loss = loss;
+    o.subset_loss = subset_loss;
+    o.status = status;
+    return pgpcv_evaluate(ctx, params, n_params, &o);
+}
+
+int pgpcv_select(pgpcv_ctx *ctx, int32_t *best, double *rmspe, int32_t *local_best, double *local_rmspe,
+                 int32_t *wins) {
+    if (!ctx) return PGPCV_EINVAL;
+    if (ctx->sel_C <= 0)
+        return ctx->fail_with(PGPCV_ESTATE, "pgpcv_select needs a preceding CV evaluation whose per-subset "
+                                            "losses are all on this device (world 1, or subset_loss requested)");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t N = ctx->N;
+    const int32_t C = ctx->sel_C;
+    CK(ctx->sel_rmspe.ensure(C), "alloc");
+    CK(ctx->sel_local.ensure((size_t)N * C), "alloc");
+    CK(ctx->sel_best.ensure(N + 1), "alloc");
+    CK(ctx->sel_wins.ensure(C), "alloc");
+    CK(launch_select(ctx->subset_loss.p, ctx->fail.p, ctx->val_off.p, ctx->sums.p, N, C, ctx->info.sum_m,
+                     ctx->sel_rmspe.p, ctx->sel_local.p, ctx->sel_best.p, ctx->sel_wins.p, st), "select");
+    if (best) CK(cudaMemcpyAsync(best, ctx->sel_best.p + N, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
+    if (rmspe) CK(cudaMemcpyAsync(rmspe, ctx->sel_rmspe.p, sizeof(double) * C, cudaMemcpyDeviceToHost, st), "copy");
+    if (local_best)
+        CK(cudaMemcpyAsync(local_best, ctx->sel_best.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st), "copy");
+    if (local_rmspe)
+        CK(cudaMemcpyAsync(local_rmspe, ctx->sel_local.p, sizeof(double) * N * C, cudaMemcpyDeviceToHost, st),
+           "copy");
+    if (wins) CK(cudaMemcpyAsync(wins, ctx->sel_wins.p, sizeof(int32_t) * C, cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaStreamSynchronize(st), "select");
+    return PGPCV_OK;
+}
+
+int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, const int32_t *subset_config,
+                  int32_t target_role, double *yhat, double *subset_sspe, double *sspe) {
+    if (!ctx) return PGPCV_EINVAL;
+    if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "pgpcv_predict needs a partition");
+    int rc = check_params(ctx, params, n_params);
+    if (rc) return rc;
+    if (target_role != PGPCV_ROLE_VALIDATION && target_role != PGPCV_ROLE_TEST)
+        return ctx->fail_with(PGPCV_EINVAL, "target_role must be PGPCV_ROLE_VALIDATION or PGPCV_ROLE_TEST");
+    const int64_t N = ctx->N;
+    if (subset_config)
+        for (int64_t s = 0; s < N; ++s)
+            if (subset_config[s] < 0 || subset_config[s] >= n_params)
+                return ctx->fail_with(PGPCV_EINVAL, "subset_config[%lld] = %d not in [0, %d)", (long long)s,
+                                      subset_config[s], n_params);
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const bool test = target_role == PGPCV_ROLE_TEST;
+    const std::vector<int64_t> &hoff = test ? ctx->h_test_off : ctx->h_val_off;
+    const int64_t n_tgt = hoff[N];
+
+    CvLaunch L;
+    L.flags = kCvPredict;
+    L.params = params;
+    L.C = n_params;
+    L.out_C = 1;
+    L.tgt_off = test ? ctx->test_off.p : ctx->val_off.p;
+    L.gx = test ? ctx->gx.p : ctx->vx.p;
+    L.gy = test ? ctx->gy.p : ctx->vy.p;
+    L.gv = test ? ctx->gv.p : ctx->vv.p;
+    for (int64_t s = 0; s < N; ++s) {
+        const int64_t k = ctx->h_train_off[s + 1] - ctx->h_train_off[s];
+        const int64_t m = hoff[s + 1] - hoff[s];
+        if (!ctx->owned[s] || m == 0) continue;
+        L.items.push_back(make_int2((int)s, subset_config ? subset_config[s] : 0));
+        const double kd = (double)k, md = (double)m;
+        L.flops += kd * kd * kd / 3.0 + kd * kd / 2.0 + kd / 6.0 + 2.0 * kd * kd + 2.0 * md * kd + 3.0 * md;
+    }
+    CK(ctx->p_sub.ensure(N), "alloc");
+    CK(ctx->p_fail.ensure(N), "alloc");
+    CK(ctx->p_yhat.ensure(std::max<int64_t>(n_tgt, 1)), "alloc");
+    CK(ctx->p_sum.ensure(1), "alloc");
+    CK(ctx->p_status.ensure(1), "alloc");
+    L.subset_loss = ctx->p_sub.p;
+    L.fail = ctx->p_fail.p;
+    L.yhat = yhat ? ctx->p_yhat.p : nullptr;
+
+    CK(cudaEventRecord(ctx->ev[0], st), "event");
+    CK(cudaMemsetAsync(ctx->p_sub.p, 0, sizeof(double) * N, st), "memset");
+    CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
+    if (yhat) CK(cudaMemsetAsync(ctx->p_yhat.p, 0, sizeof(double) * std::max<int64_t>(n_tgt, 1), st), "memset");
+    if ((rc = run_cv(ctx, L))) return rc;
+    int launches = L.items.empty() ? 0 : 1;
+    if (ctx->world > 1) {  // exclusive owners: exact sums
+        if ((rc = nccl_sum(ctx, ctx->p_sub.p, (size_t)N, ncclFloat64))) return rc;
+        if ((rc = nccl_sum(ctx, ctx->p_fail.p, (size_t)N, ncclUint8))) return rc;
+        if (yhat && n_tgt && (rc = nccl_sum(ctx, ctx->p_yhat.p, (size_t)n_tgt, ncclFloat64))) return rc;
+    }
+    CK(launch_reduce(ctx->p_sub.p, ctx->p_fail.p, L.tgt_off, N, 1, ctx->p_sum.p, ctx->p_status.p, st), "reduce");
+    ++launches;
+    double total = 0;
+    int32_t status = -1;
+    CK(cudaMemcpyAsync(&total, ctx->p_sum.p, sizeof(double), cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaMemcpyAsync(&status, ctx->p_status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
+    if (subset_sspe) CK(cudaMemcpyAsync(subset_sspe, ctx->p_sub.p, sizeof(double) * N, cudaMemcpyDeviceToHost, st), "copy");
+    if (yhat && n_tgt)
+        CK(cudaMemcpyAsync(yhat, ctx->p_yhat.p, sizeof(double) * n_tgt, cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaEventRecord(ctx->ev[3], st), "event");
+    CK(cudaStreamSynchronize(st), "predict");
+    CK(cudaGetLastError(), "predict");
+    ctx->cv_done = true;
+    record_timing(ctx, L, launches);
+    if (sspe) *sspe = total;
+    if (status >= 0) return ctx->fail_with(PGPCV_ENUMERIC, "subset %d was not positive definite", status);
+    return PGPCV_OK;
+}
+
+int pgpcv_partition_export_test(pgpcv_ctx *ctx, int64_t *test_off, int32_t *test_idx) {
+    if (!ctx) return PGPCV_EINVAL;
+    if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "no partition");
+    cudaSetDevice(ctx->device);
+    const int64_t N = ctx->N;
+    if (test_off) memcpy(test_off, ctx->h_test_off.data(), sizeof(int64_t) * (N + 1));
+    if (test_idx && ctx->info.n_test)
+        CK(cudaMemcpyAsync(test_idx, ctx->test_idx.p, sizeof(int32_t) * ctx->info.n_test, cudaMemcpyDeviceToHost,
+                           ctx->stream), "copy test_idx");
+    CK(cudaStreamSynchronize(ctx->stream), "export");
     return PGPCV_OK;
 }
 

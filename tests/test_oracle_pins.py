@@ -361,3 +361,119 @@ def test_status_reports_first_failing_subset():
     rep = oracle.cv_loss(x, y, v, part, [[0.2, 1.0, 0.0], [0.2, 1.0, 0.1]], threads=1)
     assert math.isnan(rep.loss[0]) and rep.status[0] == 0
     assert rep.status[1] == -1 and np.isfinite(rep.loss[1])
+
+
+# ----------------------------------------------------------------- row f1: grid-search consumer
+
+def _nan(v):
+    return np.array([[math.nan if e == "nan" else e for e in row] for row in v], np.float64) \
+        if isinstance(v[0], list) else np.array([math.nan if e == "nan" else e for e in v], np.float64)
+
+
+def test_select_hand_worked_golden(golden_dir):
+    """argmin / RMSPE / local winners on a hand-worked 4 x 3 case with a
+    tie, a failed (NaN) config and an empty-validation subset (tests/golden/select_small.json)."""
+    g = json.load(open(os.path.join(golden_dir, "select_small.json")))
+    best, rmspe, lb, lr, wins = oracle.select(_nan(g["loss"]), _nan(g["subset_loss"]), g["m"])
+    assert best == g["best"]
+    np.testing.assert_allclose(rmspe, _nan(g["rmspe"]), rtol=1e-15, equal_nan=True)
+    assert lb.tolist() == g["local_best"]
+    np.testing.assert_allclose(lr, _nan(g["local_rmspe"]), rtol=1e-15, equal_nan=True)
+    assert wins.tolist() == g["wins"]
+
+
+def test_test_role_partition_invariants():
+    """Test points (role 2) are listed per core tile exactly once (the held-out data the
+    chosen parameters predict); checked by an independent vectorised floor rule
+    away from tile edges, and against the validation rule applied to relabelled roles."""
+    w = workloads.make("c4", n=50_000)  # clustered layout, 80/10/10 roles (R7)
+    pt = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta, core_role=2)
+    pv = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta, core_role=1)
+    assert np.array_equal(pt.train_off, pv.train_off) and np.array_equal(pt.train_idx, pv.train_idx)
+    test = np.nonzero(w.role == 2)[0]
+    assert test.size == 5_000 and pt.val_off[-1] == test.size
+    assert np.array_equal(np.sort(pt.val_idx), test)
+    # swapping roles 1 <-> 2 turns the test lists into validation lists
+    swapped = w.role.copy()
+    swapped[w.role == 1], swapped[w.role == 2] = 2, 1
+    ps = oracle.partition(w.x, w.y, swapped, w.domain, w.kx, w.ky, w.delta, core_role=1)
+    assert np.array_equal(ps.val_off, pt.val_off) and np.array_equal(ps.val_idx, pt.val_idx)
+    # core tile by floor away from edges
+    wx = (w.domain[1] - w.domain[0]) / w.kx
+    ix = np.floor((w.x[test] - w.domain[0]) / wx).astype(int)
+    iy = np.floor((w.y[test] - w.domain[2]) / wx).astype(int)
+    s_of = np.empty(w.n, np.int64)
+    for s in range(pt.n_subsets):
+        s_of[pt.val(s)] = s
+    safe = (np.abs((w.x[test] - w.domain[0]) / wx - np.round((w.x[test] - w.domain[0]) / wx)) > 1e-9) & \
+           (np.abs((w.y[test] - w.domain[2]) / wx - np.round((w.y[test] - w.domain[2]) / wx)) > 1e-9)
+    assert np.array_equal(s_of[test][safe], (iy * w.kx + ix)[safe])
+
+
+def test_predict_yhat_closed_forms(golden_dir):
+    """The per-point predictions the oracle returns are Eq.3's yhat: k = 1 closed form
+    (golden) and k = 2 closed form, plus LAPACK cho_solve at k = 60."""
+    c = json.load(open(os.path.join(golden_dir, "closed_forms.json")))["k1"]
+    _, yh = oracle.subset_cv([c["t"][0]], [c["t"][1]], [c["y_t"]], [c["v"][0]], [c["v"][1]], [0.0],
+                             c["range"], c["sigma2"], c["nugget"], return_yhat=True)
+    assert yh[0] == pytest.approx(c["yhat"], rel=1e-14)
+    t = np.array([[0.1, 0.2], [0.4, 0.3]])
+    y1, y2 = 0.8, -1.3
+    v = np.array([0.3, 0.1])
+    theta, lam = 0.3, 0.2
+    r = math.exp(-math.dist(t[0], t[1]) / theta)
+    c1, c2 = (math.exp(-math.dist(v, t[i]) / theta) for i in range(2))
+    a = 1 + lam
+    expect = (a * (c1 * y1 + c2 * y2) - r * (c1 * y2 + c2 * y1)) / (a * a - r * r)
+    _, yh = oracle.subset_cv(t[:, 0], t[:, 1], [y1, y2], [v[0]], [v[1]], [0.0], theta, 1.0, lam,
+                             return_yhat=True)
+    assert yh[0] == pytest.approx(expect, rel=1e-13)
+    rng = np.random.default_rng(7)
+    tx, ty, tv = rng.uniform(0, 1, 60), rng.uniform(0, 1, 60), rng.normal(size=60)
+    vx, vy = rng.uniform(0, 1, 9), rng.uniform(0, 1, 9)
+    A = _cov(tx, ty, tx, ty, 0.2) + 0.1 * np.eye(60)
+    ref = _cov(vx, vy, tx, ty, 0.2) @ scipy.linalg.cho_solve(scipy.linalg.cho_factor(A, lower=True), tv)
+    _, yh = oracle.subset_cv(tx, ty, tv, vx, vy, np.zeros(9), 0.2, 1.0, 0.1, return_yhat=True)
+    np.testing.assert_allclose(yh, ref, rtol=1e-10, atol=1e-12)
+
+
+def test_predict_with_validation_targets_is_cv_loss():
+    """Predicting the validation points with one config reproduces Eq.7 per subset
+    (the per-subset SSPE is the same sum), and a per-subset config picks per-subset rows."""
+    w = workloads.make("c1")
+    part = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
+    p = np.array([[0.1, 1.0, 0.1], [0.2, 1.0, 0.05]])
+    cv = oracle.cv_loss(w.x, w.y, w.value, part, p, threads=4)
+    tot, sub, yhat = oracle.predict(w.x, w.y, w.value, part, p, threads=4)
+    assert np.array_equal(sub, cv.subset_loss[:, 0]) and tot == cv.loss[0]
+    cfg = np.array([1, 0, 1, 0])
+    _, sub2, _ = oracle.predict(w.x, w.y, w.value, part, p, subset_config=cfg, threads=4)
+    assert np.array_equal(sub2, cv.subset_loss[np.arange(4), cfg])
+    e = yhat - w.value[part.val_idx]
+    for s in range(4):
+        sl = slice(part.val_off[s], part.val_off[s + 1])
+        assert float(e[sl] @ e[sl]) == pytest.approx(sub[s], rel=1e-13)
+
+
+# ----------------------------------------------------------------- row f3: -2 log-likelihood
+
+def test_neg2loglik_composite_is_sum_of_subset_likelihoods():
+    """Per-subset -2 log L (Eq.2) over y~^i_T; with one subset (kx = ky = 1) it is
+    the full-data Gaussian likelihood (scipy multivariate_normal), and the composite is the
+    ascending-s sum of the per-subset values."""
+    rng = np.random.default_rng(3)
+    n = 150
+    x, y = rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+    v = rng.normal(size=n)
+    role = np.zeros(n, np.uint8)
+    role[::5] = 1
+    part1 = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
+    prm = np.array([[0.15, 1.7, 0.2]])
+    tot, per = oracle.neg2loglik_all(x, y, v, part1, prm, threads=2)
+    tr = role == 0
+    S = 1.7 * _cov(x[tr], y[tr], x[tr], y[tr], 0.15) + 0.2 * np.eye(int(tr.sum()))
+    ref = -2 * scipy.stats.multivariate_normal(mean=np.zeros(int(tr.sum())), cov=S).logpdf(v[tr])
+    assert tot[0] == pytest.approx(ref, rel=1e-11)
+    part4 = oracle.partition(x, y, role, (0, 1, 0, 1), 2, 2, 0.1)
+    tot4, per4 = oracle.neg2loglik_all(x, y, v, part4, prm, threads=2)
+    assert tot4[0] == per4[0, 0] + per4[1, 0] + per4[2, 0] + per4[3, 0]
