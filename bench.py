@@ -31,6 +31,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# ncu --set full capture of the dominant kernel (dram bytes per launch -> roofline.traffic)
+PROFILE_JSON = "r01_cv_kernel_v4_ncu.json"
 METRIC = "subset CV-loss evals/sec (5M pts, one (range, sigma2, nugget) config per step)"
 UNIT = "subset-evals/s"
 
@@ -117,7 +119,7 @@ def _peaks():
 
 
 def _traffic():
-    f = os.path.join(ROOT, "profiles", "r01_cv_kernel_dram.json")
+    f = os.path.join(ROOT, "profiles", PROFILE_JSON)
     if os.path.exists(f):
         try:
             return json.load(f and open(f)).get("dram_bytes_per_launch")

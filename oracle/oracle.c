@@ -284,3 +284,179 @@ int oracle_neg2loglik(int64_t k, const double *tx, const double *ty, const doubl
     free(L); free(z);
     return OR_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * Row f2: recursive shell-balanced bisection (Fig. "split" right)
+ * and the shell cap of P:418-420.  Readings (R19-R23):
+ *   - a node is a rectangle [x0,x1) x [y0,y1), closed at the domain's top edges (R3);
+ *   - depth d splits along x (a vertical line) when d is even, along y when d is odd
+ *     ("the division lines alternate"; SPEC: depth 1 = vertical line);
+ *   - counted data: training and validation points (role 0 or 1), never test points;
+ *   - "both rectangles together with their shells contain a similar amount of data"
+ *     (P:247): a child's count is the number of counted points in its L-inf dilation by
+ *     delta (R2/R3 membership: lo <= u < hi, hi = +inf at the domain top);
+ *   - candidate split lines: c = 0.5 * (u_j + u_{j+1}) for consecutive distinct values
+ *     u_j < u_{j+1} of the split coordinate of counted points in the node's core; the
+ *     one minimising |count_left - count_right| wins, ties to the smallest c (SPEC
+ *     recursive_partition); no candidate -> c = 0.5 * (x0 + x1) (R21);
+ *   - leaves are numbered in heap order: node 1 = D, children of node i are 2i (lower
+ *     coordinates) and 2i+1; subset s = leaf id - 2^depth.
+ * Plain: every count comes from scanning all n points; the candidates and band are sorted
+ * (qsort) and counted with a written-out lower bound.
+ * ------------------------------------------------------------------------- */
+
+static int in_dil(double u, double lo, double hi, double top, double delta) {
+    double l = lo - delta;
+    double h = (hi == top) ? INFINITY : hi + delta;
+    return l <= u && u < h;
+}
+static int in_core(double u, double lo, double hi, double top) {
+    return lo <= u && (u < hi || (hi == top && u == top));
+}
+static int cmp_double(const void *a, const void *b) {
+    double x = *(const double *)a, y = *(const double *)b;
+    return (x > y) - (x < y);
+}
+/* number of entries of the sorted array a[0..len) that are < v */
+static int64_t count_below(const double *a, int64_t len, double v) {
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+/* rects: [2^depth * 4] (x0, x1, y0, y1) per leaf; splits: [2^depth] split coordinate of
+ * node id (index id, id = 1 .. 2^depth - 1; entry 0 unused). */
+int oracle_bisect(int64_t n, const double *x, const double *y, const uint8_t *role,
+                  double xmin, double xmax, double ymin, double ymax, int32_t depth, double delta,
+                  double *rects, double *splits) {
+    if (depth < 0 || depth > 20 || !(delta >= 0.0) || isinf(delta)) return OR_EINVAL;
+    int rc = check_inputs(n, x, y, role, xmin, xmax, ymin, ymax, 1, 1, delta);
+    if (rc) return rc;
+    int64_t nodes = (int64_t)1 << (depth + 1);
+    double *R = malloc(sizeof(double) * 4 * (size_t)nodes); /* rect of node id */
+    double *band = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *core = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    if (!R || !band || !core) { free(R); free(band); free(core); return OR_ENOMEM; }
+    R[4] = xmin; R[5] = xmax; R[6] = ymin; R[7] = ymax;
+    for (int32_t d = 0; d < depth; ++d) {
+        int axis = d & 1; /* 0: split x, 1: split y */
+        for (int64_t id = (int64_t)1 << d; id < ((int64_t)1 << (d + 1)); ++id) {
+            const double *r = R + 4 * id;
+            int64_t nb = 0, nc = 0;
+            for (int64_t p = 0; p < n; ++p) {
+                if (role[p] > 1) continue;
+                int dx = in_dil(x[p], r[0], r[1], xmax, delta), dy = in_dil(y[p], r[2], r[3], ymax, delta);
+                if (dx && dy) band[nb++] = axis ? y[p] : x[p];
+                if (in_core(x[p], r[0], r[1], xmax) && in_core(y[p], r[2], r[3], ymax))
+                    core[nc++] = axis ? y[p] : x[p];
+            }
+            qsort(band, (size_t)nb, sizeof(double), cmp_double);
+            qsort(core, (size_t)nc, sizeof(double), cmp_double);
+            double best_c = 0.5 * (r[2 * axis] + r[2 * axis + 1]);
+            int64_t best_score = -1;
+            for (int64_t j = 0; j + 1 < nc; ++j) {
+                if (!(core[j] < core[j + 1])) continue;
+                double c = 0.5 * (core[j] + core[j + 1]);
+                int64_t left = count_below(band, nb, c + delta);        /* u <  c + delta */
+                int64_t right = nb - count_below(band, nb, c - delta);  /* u >= c - delta */
+                int64_t score = left > right ? left - right : right - left;
+                if (best_score < 0 || score < best_score) { best_score = score; best_c = c; }
+            }
+            splits[id] = best_c;
+            double *lc = R + 4 * (2 * id), *rc2 = R + 4 * (2 * id + 1);
+            for (int i = 0; i < 4; ++i) { lc[i] = r[i]; rc2[i] = r[i]; }
+            lc[2 * axis + 1] = best_c; /* left/lower child ends at c */
+            rc2[2 * axis] = best_c;    /* right/upper child starts at c */
+        }
+    }
+    for (int64_t s = 0; s < ((int64_t)1 << depth); ++s)
+        for (int i = 0; i < 4; ++i) rects[4 * s + i] = R[4 * (((int64_t)1 << depth) + s) + i];
+    if (depth == 0) splits[0] = 0.0;
+    free(R); free(band); free(core);
+    return OR_OK;
+}
+
+/* Membership for an arbitrary list of N leaf rectangles (brute force over all rects):
+ * train(s) = role 0 in the dilation of rect s; core(s) = role core_role in rect s. */
+int oracle_partition_rects_count(int64_t n, const double *x, const double *y, const uint8_t *role,
+                                 double xmax, double ymax, int64_t N, const double *rects,
+                                 double delta, uint8_t core_role, int64_t *train_cnt, int64_t *val_cnt) {
+    for (int64_t s = 0; s < N; ++s) { train_cnt[s] = 0; val_cnt[s] = 0; }
+    for (int64_t p = 0; p < n; ++p)
+        for (int64_t s = 0; s < N; ++s) {
+            const double *r = rects + 4 * s;
+            if (role[p] == 0 && in_dil(x[p], r[0], r[1], xmax, delta) && in_dil(y[p], r[2], r[3], ymax, delta))
+                train_cnt[s] += 1;
+            if (role[p] == core_role && in_core(x[p], r[0], r[1], xmax) && in_core(y[p], r[2], r[3], ymax))
+                val_cnt[s] += 1;
+        }
+    return OR_OK;
+}
+
+int oracle_partition_rects_fill(int64_t n, const double *x, const double *y, const uint8_t *role,
+                                double xmax, double ymax, int64_t N, const double *rects, double delta,
+                                uint8_t core_role, const int64_t *train_off, int32_t *train_idx,
+                                const int64_t *val_off, int32_t *val_idx) {
+    int64_t *tpos = malloc(sizeof(int64_t) * (size_t)(N > 0 ? N : 1));
+    int64_t *vpos = malloc(sizeof(int64_t) * (size_t)(N > 0 ? N : 1));
+    if (!tpos || !vpos) { free(tpos); free(vpos); return OR_ENOMEM; }
+    for (int64_t s = 0; s < N; ++s) { tpos[s] = train_off[s]; vpos[s] = val_off[s]; }
+    for (int64_t p = 0; p < n; ++p) /* ascending p: every list ends up in ascending index */
+        for (int64_t s = 0; s < N; ++s) {
+            const double *r = rects + 4 * s;
+            if (role[p] == 0 && in_dil(x[p], r[0], r[1], xmax, delta) && in_dil(y[p], r[2], r[3], ymax, delta))
+                train_idx[tpos[s]++] = (int32_t)p;
+            if (role[p] == core_role && in_core(x[p], r[0], r[1], xmax) && in_core(y[p], r[2], r[3], ymax))
+                val_idx[vpos[s]++] = (int32_t)p;
+        }
+    free(tpos); free(vpos);
+    return OR_OK;
+}
+
+/* SplitMix64 (Steele, Lea & Flood 2014): output i >= 1 of the generator seeded with
+ * `seed` is mix(seed + i * 0x9e3779b97f4a7c15). */
+uint64_t oracle_splitmix64(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + i * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+/* Shell cap (shells with more than 2,000 residuals are reduced "to 2,000 by
+ * random sampling"; reading R22): of subset s's training list (ascending p) the shell
+ * members -- those outside the core rect -- are kept only if their key
+ * splitmix64(seed, s * 2^32 + p + 1) is among the `cap` smallest (ties: smaller p);
+ * core members are always kept.  Writes the kept list (ascending p) to out, its length
+ * to *k_out. */
+int oracle_cap_shell(int64_t k, const int32_t *idx, const double *x, const double *y, const double *rect,
+                     double xmax, double ymax, int64_t cap, uint64_t seed, int64_t s, int32_t *out,
+                     int64_t *k_out) {
+    int64_t nshell = 0;
+    for (int64_t i = 0; i < k; ++i) {
+        int32_t p = idx[i];
+        if (!(in_core(x[p], rect[0], rect[1], xmax) && in_core(y[p], rect[2], rect[3], ymax))) ++nshell;
+    }
+    for (int64_t i = 0, o = 0; i < k; ++i) {
+        int32_t p = idx[i];
+        int keep = 1;
+        if (nshell > cap && !(in_core(x[p], rect[0], rect[1], xmax) && in_core(y[p], rect[2], rect[3], ymax))) {
+            /* rank of p among the shell members by (key, p): keep iff rank < cap */
+            uint64_t kp = oracle_splitmix64(seed, ((uint64_t)s << 32) + (uint64_t)p + 1);
+            int64_t rank = 0;
+            for (int64_t j = 0; j < k; ++j) {
+                int32_t q = idx[j];
+                if (in_core(x[q], rect[0], rect[1], xmax) && in_core(y[q], rect[2], rect[3], ymax)) continue;
+                uint64_t kq = oracle_splitmix64(seed, ((uint64_t)s << 32) + (uint64_t)q + 1);
+                if (kq < kp || (kq == kp && q < p)) ++rank;
+            }
+            keep = rank < cap;
+        }
+        if (keep) out[o++] = p;
+        if (i == k - 1) *k_out = o;
+    }
+    if (k == 0) *k_out = 0;
+    return OR_OK;
+}
