@@ -59,6 +59,13 @@ def _load():
             for f in (lib.oracle_subset_cv, lib.oracle_subset_cv_ld):
                 f.argtypes = [i64, p, p, p, i64, p, p, p, d, d, d, p, p]
             lib.oracle_neg2loglik.argtypes = [i64, p, p, p, d, d, d, p]
+            u64 = ctypes.c_uint64
+            lib.oracle_bisect.argtypes = [i64, p, p, p, d, d, d, d, i32, d, p, p]
+            lib.oracle_partition_rects_count.argtypes = [i64, p, p, p, d, d, i64, p, d, u8, p, p]
+            lib.oracle_partition_rects_fill.argtypes = [i64, p, p, p, d, d, i64, p, d, u8, p, p, p, p]
+            lib.oracle_splitmix64.argtypes = [u64, u64]
+            lib.oracle_splitmix64.restype = u64
+            lib.oracle_cap_shell.argtypes = [i64, p, p, p, p, d, d, i64, u64, i64, p, p]
             _lib = lib
     return _lib
 
@@ -330,3 +337,85 @@ def predict(x, y, v, part: Partition, params, subset_config=None, threads: int |
     for s in range(N):
         total = total + float(sub[s])
     return total, sub, yhat
+
+
+# ----------------------------------------------------------------- row f2: bisection
+
+class RectPartition(Partition):
+    """Partition over an explicit list of N leaf rectangles (x0, x1, y0, y1)."""
+
+    def __init__(self, train_off, train_idx, val_off, val_idx, rects):
+        super().__init__(train_off, train_idx, val_off, val_idx, len(rects), 1)
+        self.rects = rects
+
+
+def bisect(x, y, role, domain, depth: int, delta: float):
+    """Recursive shell-balanced bisection of D into 2^depth rectangles (readings
+    R19-R21 in oracle.c).  Returns (splits[2^depth] by node id, rects[2^depth, 4])."""
+    lib = _load()
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    role = np.ascontiguousarray(role, np.uint8)
+    N = 1 << depth
+    rects = np.zeros((N, 4), np.float64)
+    splits = np.zeros(N, np.float64)
+    xmin, xmax, ymin, ymax = (float(v) for v in domain)
+    rc = lib.oracle_bisect(x.shape[0], _ptr(x), _ptr(y), _ptr(role), xmin, xmax, ymin, ymax, int(depth),
+                           float(delta), _ptr(rects), _ptr(splits))
+    if rc:
+        raise OracleError(rc, "bisect")
+    return splits, rects
+
+
+def partition_rects(x, y, role, domain, rects, delta: float, core_role: int = 1) -> RectPartition:
+    """Brute-force membership over leaf rectangles: training = role 0 in the dilation by
+    delta (R2/R3), core lists = role core_role in the rectangle; ascending index."""
+    lib = _load()
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    role = np.ascontiguousarray(role, np.uint8)
+    rects = np.ascontiguousarray(rects, np.float64).reshape(-1, 4)
+    N = rects.shape[0]
+    xmax, ymax = float(domain[1]), float(domain[3])
+    tc = np.zeros(N, np.int64)
+    vc = np.zeros(N, np.int64)
+    lib.oracle_partition_rects_count(x.shape[0], _ptr(x), _ptr(y), _ptr(role), xmax, ymax, N, _ptr(rects),
+                                     float(delta), int(core_role), _ptr(tc), _ptr(vc))
+    toff = np.zeros(N + 1, np.int64)
+    voff = np.zeros(N + 1, np.int64)
+    np.cumsum(tc, out=toff[1:])
+    np.cumsum(vc, out=voff[1:])
+    tidx = np.empty(int(toff[-1]), np.int32)
+    vidx = np.empty(int(voff[-1]), np.int32)
+    lib.oracle_partition_rects_fill(x.shape[0], _ptr(x), _ptr(y), _ptr(role), xmax, ymax, N, _ptr(rects),
+                                    float(delta), int(core_role), _ptr(toff), _ptr(tidx), _ptr(voff), _ptr(vidx))
+    return RectPartition(toff, tidx, voff, vidx, rects)
+
+
+def splitmix64(seed: int, i: int) -> int:
+    """Output i >= 1 of SplitMix64 seeded with ``seed`` (the shell-cap sampling keys)."""
+    return int(_load().oracle_splitmix64(seed & (2**64 - 1), i & (2**64 - 1)))
+
+
+def cap_shells(part: RectPartition, x, y, domain, cap: int, seed: int) -> RectPartition:
+    """Shell cap (reading R22): in every subset whose shell (training points
+    outside the core rectangle) exceeds ``cap``, keep the ``cap`` shell members with the
+    smallest SplitMix64 keys (ties: smaller index); the core part is kept whole."""
+    lib = _load()
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    xmax, ymax = float(domain[1]), float(domain[3])
+    N = part.n_subsets
+    lists = []
+    for s in range(N):
+        idx = np.ascontiguousarray(part.train(s), np.int32)
+        out = np.empty(max(idx.size, 1), np.int32)
+        kout = np.zeros(1, np.int64)
+        rect = np.ascontiguousarray(part.rects[s], np.float64)
+        lib.oracle_cap_shell(idx.size, _ptr(idx), _ptr(x), _ptr(y), _ptr(rect), xmax, ymax, int(cap),
+                             seed & (2**64 - 1), s, _ptr(out), _ptr(kout))
+        lists.append(out[:int(kout[0])].copy())
+    toff = np.zeros(N + 1, np.int64)
+    np.cumsum([l.size for l in lists], out=toff[1:])
+    tidx = np.concatenate(lists) if lists else np.empty(0, np.int32)
+    return RectPartition(toff, tidx.astype(np.int32), part.val_off, part.val_idx, part.rects)

@@ -477,3 +477,135 @@ def test_neg2loglik_composite_is_sum_of_subset_likelihoods():
     part4 = oracle.partition(x, y, role, (0, 1, 0, 1), 2, 2, 0.1)
     tot4, per4 = oracle.neg2loglik_all(x, y, v, part4, prm, threads=2)
     assert tot4[0] == per4[0, 0] + per4[1, 0] + per4[2, 0] + per4[3, 0]
+
+
+# ----------------------------------------------------------------- row f2: bisection, shell cap
+
+def _bisect_numpy(x, y, role, domain, depth, delta):
+    """Independent brute force of the same rule (R19-R21): every candidate split of every
+    node is counted with boolean masks over all points (no sorting, no binary search)."""
+    xmin, xmax, ymin, ymax = domain
+    counted = role <= 1
+    rects = {1: (xmin, xmax, ymin, ymax)}
+    splits = {}
+
+    def dil(u, lo, hi, top):
+        h = np.inf if hi == top else hi + delta
+        return (lo - delta <= u) & (u < h)
+
+    def core(u, lo, hi, top):
+        return (lo <= u) & ((u < hi) | ((hi == top) & (u == top)))
+
+    for d in range(depth):
+        ax = d & 1
+        for nid in range(1 << d, 1 << (d + 1)):
+            x0, x1, y0, y1 = rects[nid]
+            u = y if ax else x
+            lo, hi, top = (y0, y1, ymax) if ax else (x0, x1, xmax)
+            other = dil(x, x0, x1, xmax) if ax else dil(y, y0, y1, ymax)
+            incore = counted & core(x, x0, x1, xmax) & core(y, y0, y1, ymax)
+            vals = np.unique(u[incore])
+            best, bc = None, 0.5 * (lo + hi)
+            for j in range(vals.size - 1):
+                c = 0.5 * (vals[j] + vals[j + 1])
+                left = int(np.sum(counted & other & (lo - delta <= u) & (u < c + delta)))
+                right = int(np.sum(counted & other & (c - delta <= u) & (u < (np.inf if hi == top else hi + delta))))
+                sc = abs(left - right)
+                if best is None or sc < best:
+                    best, bc = sc, c
+            splits[nid] = bc
+            r = list(rects[nid])
+            lc, rc = list(r), list(r)
+            lc[2 * ax + 1] = bc
+            rc[2 * ax] = bc
+            rects[2 * nid], rects[2 * nid + 1] = tuple(lc), tuple(rc)
+    leaves = np.array([rects[(1 << depth) + s] for s in range(1 << depth)])
+    return splits, leaves
+
+
+def test_bisect_spec_example_median_split():
+    """q = 1, delta = 0, 10 points with distinct x: the split lies midway between the 5th
+    and 6th smallest x and leaves 5 / 5 (SPEC recursive_partition example)."""
+    rng = np.random.default_rng(11)
+    x, y = rng.uniform(0, 1, 10), rng.uniform(0, 1, 10)
+    splits, rects = oracle.bisect(x, y, np.zeros(10, np.uint8), (0, 1, 0, 1), 1, 0.0)
+    xs = np.sort(x)
+    assert splits[1] == 0.5 * (xs[4] + xs[5])
+    assert rects.tolist() == [[0, splits[1], 0, 1], [splits[1], 1, 0, 1]]
+
+
+@pytest.mark.parametrize("depth,delta", [(1, 0.0), (2, 0.1), (3, 0.05), (4, 0.02)])
+def test_bisect_matches_independent_brute_force(depth, delta):
+    """Splits and leaves equal (bit for bit) a boolean-mask brute force of the rule, with
+    test-role points present (they never count, R20)."""
+    x, y, v, role = workloads.random_points(20 + depth, 160, frac_val=0.2, frac_test=0.1)
+    splits, rects = oracle.bisect(x, y, role, (0, 1, 0, 1), depth, delta)
+    ref_splits, ref_rects = _bisect_numpy(x, y, role, (0, 1, 0, 1), depth, delta)
+    for nid, c in ref_splits.items():
+        assert splits[nid] == c, nid
+    assert np.array_equal(rects, ref_rects)
+
+
+def test_bisect_structure_and_balance():
+    """Leaves tile D (every point in exactly one core), axes alternate (even depths split
+    x), and with delta = 0 and distinct coordinates every split is balanced to one point."""
+    x, y, v, role = workloads.random_points(5, 3000, frac_val=0.1, frac_test=0.1)
+    depth = 5
+    splits, rects = oracle.bisect(x, y, role, (0, 1, 0, 1), depth, 0.0)
+    part = oracle.partition_rects(x, y, np.zeros_like(role), (0, 1, 0, 1), rects, 0.0, core_role=0)
+    assert part.train_off[-1] == x.size  # delta = 0: train lists partition all points
+    counted = (role <= 1)
+    per_leaf = np.array([counted[part.train(s)].sum() for s in range(1 << depth)])
+    # sibling leaves (and recursively every split) balance to within one point
+    level = per_leaf
+    while level.size > 1:
+        assert np.all(np.abs(level[0::2] - level[1::2]) <= 1)
+        level = level[0::2] + level[1::2]
+    for s in range(1 << depth):
+        x0, x1, y0, y1 = rects[s]
+        assert x0 < x1 and y0 < y1
+    # depth-0 split is a vertical line: the two halves of the leaf list share x ranges
+    assert np.all(rects[: 1 << (depth - 1), 1] <= splits[1]) and np.all(rects[1 << (depth - 1):, 0] >= splits[1])
+
+
+def test_rect_membership_equals_grid_membership():
+    """The rectangle-list membership with the grid's tiles as rectangles is the grid
+    partition bit for bit (two independent routines of R2-R5)."""
+    w = workloads.make("c2")
+    ex, ey = oracle.edges(0.0, 1.0, w.kx), oracle.edges(0.0, 1.0, w.ky)
+    rects = np.array([[ex[i], ex[i + 1], ey[j], ey[j + 1]] for j in range(w.ky) for i in range(w.kx)])
+    g = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
+    r = oracle.partition_rects(w.x, w.y, w.role, w.domain, rects, w.delta)
+    for a in ("train_off", "train_idx", "val_off", "val_idx"):
+        assert np.array_equal(getattr(g, a), getattr(r, a)), a
+
+
+def test_splitmix64_reference_vector():
+    """SplitMix64 seeded with 0: the published first outputs (Vigna's splitmix64.c)."""
+    assert oracle.splitmix64(0, 1) == 0xE220A8397B1DCDAF
+    assert oracle.splitmix64(0, 2) == 0x6E789E6AA1B965F4
+    assert oracle.splitmix64(0, 3) == 0x06C45D188009454F
+
+
+def test_shell_cap_rules():
+    """cap >= every shell: unchanged; cap = 0: only the core training points (= the
+    delta = 0 lists); otherwise min(shell, cap) shell points kept, core whole, a subset of
+    the original list, deterministic in the seed and dependent on it."""
+    x, y, v, role = workloads.random_points(9, 4000, frac_val=0.1)
+    D = (0, 1, 0, 1)
+    _, rects = oracle.bisect(x, y, role, D, 3, 0.08)
+    part = oracle.partition_rects(x, y, role, D, rects, 0.08)
+    big = oracle.cap_shells(part, x, y, D, 10**6, 1)
+    assert np.array_equal(big.train_idx, part.train_idx)
+    zero = oracle.cap_shells(part, x, y, D, 0, 1)
+    core_only = oracle.partition_rects(x, y, role, D, rects, 0.0)
+    assert np.array_equal(zero.train_off, core_only.train_off) and np.array_equal(zero.train_idx, core_only.train_idx)
+    cap = 60
+    a = oracle.cap_shells(part, x, y, D, cap, 123)
+    b = oracle.cap_shells(part, x, y, D, cap, 123)
+    c = oracle.cap_shells(part, x, y, D, cap, 124)
+    assert np.array_equal(a.train_idx, b.train_idx) and not np.array_equal(a.train_idx, c.train_idx)
+    for s in range(8):
+        full, kept, core = set(part.train(s)), a.train(s), set(core_only.train(s))
+        assert np.all(np.diff(kept) > 0) and set(kept) <= full and core <= set(kept)
+        assert len(set(kept) - core) == min(len(full - core), cap)
