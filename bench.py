@@ -34,6 +34,10 @@ sys.path.insert(0, ROOT)
 # ncu --set full capture of the dominant kernel (dram bytes per launch -> roofline.traffic)
 PROFILE_JSON = "r01_cv_kernel_v4_ncu.json"
 METRIC = "subset CV-loss evals/sec (5M pts, one (range, sigma2, nugget) config per step)"
+METRICS = {"cv": METRIC,
+           "cv_nll": "subset CV-loss + -2 log-lik evals/sec (one factorization, one config per step)",
+           "nll": "subset -2 log-likelihood evals/sec (one config per step)",
+           "predict": "subset test-set kriging evals/sec (one config per step)"}
 UNIT = "subset-evals/s"
 
 
@@ -143,12 +147,11 @@ def run_reference(args, rank, world):
     host cores, on the same workload/metric; rank 0 only."""
     if rank != 0:
         return 0
-    import oracle
     import workloads
 
     dev = "cuda" if _has_cuda() else "cpu"
     w = workloads.make(args.workload, device=dev)
-    part = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
+    part = _oracle_partition(w, core_role=2 if args.mode == "predict" else 1)
     k, m = part.k(), part.m()
     cores = os.cpu_count() or 1
     sample = _stratified_sample(k, m, cores)
@@ -156,7 +159,7 @@ def run_reference(args, rank, world):
     for step in range(args.warmup + args.steps):
         p = w.params[step % len(w.params)][None, :]
         t0 = time.perf_counter()
-        oracle.cv_loss(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
+        _oracle_step(w, part, p, sample, cores, args.mode)
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             t_total += dt
@@ -165,9 +168,9 @@ def run_reference(args, rank, world):
     desc = (f"{sample.size} stratified {args.workload} subsets (k {int(k[sample].min())}-"
             f"{int(k[sample].max())}) x 1 config per step, oracle.c (-O2, no FMA) as it stands")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": METRICS[args.mode], "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": _config(args, w, part),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -186,9 +189,13 @@ def _config(args, w, part_or_info):
         N, nv = part_or_info["n_subsets"], part_or_info["n_val"]
     else:
         N, nv = part_or_info.n_subsets, int(part_or_info.m().sum())
+    div = (f"{w.kx}x{w.ky} tiles" if w.depth is None else
+           f"recursive bisection into 2^{w.depth} subsets, shell cap {w.shell_cap}")
+    mode = {"cv": "", "cv_nll": ", CV loss + per-subset -2 log-lik (one factorization)",
+            "nll": ", per-subset -2 log-lik only", "predict": ", test-set kriging prediction"}[args.mode]
     return {"workload": f"{args.workload}: n={w.n:,} on [{w.domain[0]:g},{w.domain[1]:g}]^2, "
-                        f"{w.kx}x{w.ky} tiles, delta={w.delta:g}, {len(w.params)}-config grid "
-                        f"(one config per step), FP64",
+                        f"{div}, delta={w.delta:g}, {len(w.params)}-config grid "
+                        f"(one config per step){mode}, FP64",
             "n_points": w.n, "n_subsets": N, "n_val": nv, "grid_configs": len(w.params),
             "configs_per_step": 1, "parallelism": f"subsets sharded by LPT over {args.gpus} GPU(s)",
             "l2": "no flush: per-step factor working set (148 slots x up to 142 MB) >> 126 MB L2"}
@@ -217,7 +224,17 @@ def run_ours(args, rank, world, local_rank):
     ctx = pg.Context(local_rank)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    info = ctx.partition_device(dx, dy, dv, dr, w.domain, w.kx, w.ky, w.delta)
+    def part_device():
+        if w.depth is None:
+            return ctx.partition_device(dx, dy, dv, dr, w.domain, w.kx, w.ky, w.delta)
+        return ctx.partition_bisect_device(dx, dy, dv, dr, w.domain, w.depth, w.delta, w.shell_cap, w.cap_seed)
+
+    def part_host():
+        if w.depth is None:
+            return ctx.partition(hx, hy, hv, hr, w.domain, w.kx, w.ky, w.delta)
+        return ctx.partition_bisect(hx, hy, hv, hr, w.domain, w.depth, w.delta, w.shell_cap, w.cap_seed)
+
+    info = part_device()
     uid = None
     if world > 1:
         obj = [pg.nccl_unique_id() if rank == 0 else None]
@@ -225,11 +242,22 @@ def run_ours(args, rank, world, local_rank):
         uid = obj[0]
     ctx.shard(rank, world, uid)
     toff, _, voff, _ = ctx.partition_export()
-    kk, mm = np.diff(toff), np.diff(voff)
-    evals_per_step = int((mm > 0).sum())  # all subsets with validation data, over all ranks
+    goff, _ = ctx.partition_export_test()
+    kk, mm, gg = np.diff(toff), np.diff(voff), np.diff(goff)
+    # (subset, config) evaluations per step over all ranks: subsets with validation data
+    # (cv), every subset (the likelihood needs no targets), subsets with test points (predict)
+    evals_per_step = {"cv": int((mm > 0).sum()), "cv_nll": int(kk.size), "nll": int(kk.size),
+                      "predict": int((gg > 0).sum())}[args.mode]
 
     def step(i):
-        return ctx.cv_loss(w.params[i % C][None, :], want_subset_loss=False)
+        p = w.params[i % C][None, :]
+        if args.mode == "cv":
+            return ctx.cv_loss(p, want_subset_loss=False).loss[0]
+        if args.mode == "cv_nll":
+            return ctx.evaluate(p, subset_loss=False, nll=True).loss[0]
+        if args.mode == "nll":
+            return ctx.evaluate(p, loss=False, subset_loss=False, nll=True).nll[0]
+        return ctx.predict(p, want_yhat=False).sspe
 
     for i in range(args.warmup):
         step(i)
@@ -252,7 +280,7 @@ def run_ours(args, rank, world, local_rank):
         kern_ms += t["kernel_ms"]
         kern_flops += t["flops"]
         launches += t["launches"]
-        losses.append(float(r.loss[0]))
+        losses.append(float(r))
     e1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -269,8 +297,8 @@ def run_ours(args, rank, world, local_rank):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for i in range(args.steps):
-        ctx.partition(hx, hy, hv, hr, w.domain, w.kx, w.ky, w.delta)
-        ctx.cv_loss(w.params[(args.warmup + i) % C][None, :], want_subset_loss=False)
+        part_host()
+        step(args.warmup + i)
     f1.record(stream)
     barrier()
     e2e_ms = f0.elapsed_time(f1)
@@ -285,7 +313,7 @@ def run_ours(args, rank, world, local_rank):
     value = evals_per_step * args.steps / (t_ms * 1e-3)
     n = w.n
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRICS[args.mode], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(args, w, info),
@@ -307,7 +335,7 @@ def run_ours(args, rank, world, local_rank):
         "loss_first_step": losses[0],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = _cpu_baseline(w, toff, voff, args)
+        line["cpu_baseline"] = _cpu_baseline(w, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -316,19 +344,42 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
-def _cpu_baseline(w, toff, voff, args):
-    """The oracle as it stands on the host cores: a bounded sample of the same workload
-    (one c5 subset per core x 1 config, ~15 s), scaled to evals/s."""
+def _oracle_partition(w, core_role=1):
+    """The oracle's own membership (independent of the GPU): brute-force tiles, or the
+    oracle's bisection + rectangle membership + shell cap for c6."""
     import oracle
 
-    part = oracle.Partition(toff, None, voff, None, w.kx, w.ky)
-    # membership lists from the oracle's own brute-force partition (independent of the GPU)
-    part = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
+    if w.depth is None:
+        return oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta, core_role=core_role)
+    _, rects = oracle.bisect(w.x, w.y, w.role, w.domain, w.depth, w.delta)
+    part = oracle.partition_rects(w.x, w.y, w.role, w.domain, rects, w.delta, core_role=core_role)
+    return oracle.cap_shells(part, w.x, w.y, w.domain, w.shell_cap, w.cap_seed) if w.shell_cap >= 0 else part
+
+
+def _oracle_step(w, part, p, sample, cores, mode):
+    """One bounded oracle step of the bench's mode on `sample` subsets."""
+    import oracle
+
+    if mode in ("cv", "cv_nll"):
+        oracle.cv_loss(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
+    if mode in ("cv_nll", "nll"):
+        oracle.neg2loglik_all(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
+    if mode == "predict":  # part holds the test lists as its core lists
+        sub = oracle.Partition(part.train_off, part.train_idx, part.val_off, part.val_idx, part.n_subsets, 1)
+        keep = np.zeros(part.n_subsets, bool)
+        keep[sample] = True
+        oracle.cv_loss(w.x, w.y, w.value, sub, p, subsets=np.nonzero(keep)[0], threads=cores)
+
+
+def _cpu_baseline(w, args):
+    """The oracle as it stands on the host cores: a bounded sample of the same workload
+    (one subset per core x 1 config, ~15 s at c5), scaled to evals/s."""
+    part = _oracle_partition(w, core_role=2 if args.mode == "predict" else 1)
     cores = os.cpu_count() or 1
     sample = _stratified_sample(part.k(), part.m(), cores)
     p = w.params[args.warmup % len(w.params)][None, :]
     t0 = time.perf_counter()
-    oracle.cv_loss(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
+    _oracle_step(w, part, p, sample, cores, args.mode)
     dt = time.perf_counter() - t0
     return {"value": sample.size / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{sample.size} stratified {args.workload} subsets x 1 config "
@@ -342,7 +393,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
+    ap.add_argument("--mode", default="cv", choices=["cv", "cv_nll", "nll", "predict"],
+                    help="cv: the headline CV loss; cv_nll / nll: row f3; predict: row f1 test-set kriging")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)

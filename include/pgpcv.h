@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PGPCV_VERSION 2
+#define PGPCV_VERSION 3
 
 /* Error codes. */
 #define PGPCV_OK 0
@@ -158,6 +158,40 @@ int pgpcv_partition_device(pgpcv_ctx *ctx, int64_t n, const double *d_x, const d
                            const double *d_value, const uint8_t *d_role, pgpcv_rect domain,
                            int32_t kx, int32_t ky, double delta,
                            pgpcv_partition_info *info_out);
+
+/* Row f2: the paper's own division -- recursive shell-balanced bisection of D
+ * into N = 2^depth rectangles, then the same membership rules as pgpcv_partition (training
+ * = role 0 in the rectangle's L-inf dilation by delta, validation/test = role 1/2 in the
+ * rectangle).  Node 1 is D; a node at depth d is split along x (d even) or y (d odd) by the
+ * line c minimising |count_left - count_right|, a child's count being the number of role 0
+ * and role 1 points in its dilation by delta ("both rectangles together with their shells
+ * contain a similar amount of data"); candidates are c = 0.5 (u_j + u_{j+1}) over
+ * consecutive distinct split coordinates of counted points in the node, ties to the
+ * smallest c, no candidate -> the node's midpoint (R19-R21).  Subset s is leaf
+ * 2^depth + s of the heap-numbered tree (left = lower coordinates).
+ *   depth: 0..20.
+ *   shell_cap: < 0 for none; else, in every subset whose shell (training points outside
+ *     its rectangle) exceeds shell_cap, keep the shell_cap shell points with the smallest
+ *     keys splitmix64(seed, s * 2^32 + p + 1) (ties: smaller p), as the paper's 5M-point
+ *     fit reduces shells to 2,000 "by random sampling" (R22).
+ * Bit-exact and deterministic (exact FP64 comparisons, single correctly rounded ops).
+ * Errors: EINVAL, ECUDA, ENOMEM. */
+int pgpcv_partition_bisect(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y,
+                           const double *value, const uint8_t *role, pgpcv_rect domain,
+                           int32_t depth, double delta, int64_t shell_cap, uint64_t seed,
+                           pgpcv_partition_info *info_out);
+
+/* Same with x, y, value, role in device memory of the ctx device. */
+int pgpcv_partition_bisect_device(pgpcv_ctx *ctx, int64_t n, const double *d_x,
+                                  const double *d_y, const double *d_value,
+                                  const uint8_t *d_role, pgpcv_rect domain, int32_t depth,
+                                  double delta, int64_t shell_cap, uint64_t seed,
+                                  pgpcv_partition_info *info_out);
+
+/* The N subset rectangles of the current partition, (x0, x1, y0, y1) per subset into the
+ * caller's double[4*N] (tiles for pgpcv_partition, leaves for the bisection).
+ * Errors: EINVAL (NULL), ESTATE (no partition). */
+int pgpcv_partition_rects(pgpcv_ctx *ctx, double *rects);
 
 /* Copy the CSR membership of the current partition to caller-allocated host arrays:
  * train_off int64[N+1], train_idx int32[sum_k], val_off int64[N+1], val_idx int32[sum_m]

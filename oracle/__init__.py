@@ -66,6 +66,8 @@ def _load():
             lib.oracle_splitmix64.argtypes = [u64, u64]
             lib.oracle_splitmix64.restype = u64
             lib.oracle_cap_shell.argtypes = [i64, p, p, p, p, d, d, i64, u64, i64, p, p]
+            lib.oracle_gls_subset.argtypes = [i64, p, p, p, p, p, i32, d, d, d, p, p]
+            lib.oracle_solve_small.argtypes = [i32, p, p, p]
             _lib = lib
     return _lib
 
@@ -419,3 +421,55 @@ def cap_shells(part: RectPartition, x, y, domain, cap: int, seed: int) -> RectPa
     np.cumsum([l.size for l in lists], out=toff[1:])
     tidx = np.concatenate(lists) if lists else np.empty(0, np.int32)
     return RectPartition(toff, tidx.astype(np.int32), part.val_off, part.val_idx, part.rects)
+
+
+# ----------------------------------------------------------------- row f4: GLS
+
+def gls(x, y, v, X, part, rects, domain, param, subsets=None, threads: int | None = None):
+    """Row f4 (Eq. GLS; reading R23): beta_hat = A^{-1} b with
+    A = sum_s sum_{p in core_s} X_p^T (M_s^{-1} X^s)_p and b likewise with y, summed over
+    subsets in ascending s; ``part`` gives the training lists, ``rects`` the cores (a
+    training point is in core s iff it lies in rectangle s, R3).  Returns (beta, A, b)."""
+    lib = _load()
+    X = np.ascontiguousarray(X, np.float64)
+    p = X.shape[1]
+    rects = np.asarray(rects, np.float64).reshape(-1, 4)
+    xmax, ymax = float(domain[1]), float(domain[3])
+    N = part.n_subsets
+    sub = np.arange(N) if subsets is None else np.asarray(subsets, np.int64)
+    As = np.zeros((N, p, p))
+    bs = np.zeros((N, p))
+
+    def core_mask(s, ti):
+        x0, x1, y0, y1 = rects[s]
+        cx = (x0 <= x[ti]) & ((x[ti] < x1) | ((x1 == xmax) & (x[ti] == xmax)))
+        cy = (y0 <= y[ti]) & ((y[ti] < y1) | ((y1 == ymax) & (y[ti] == ymax)))
+        return np.ascontiguousarray(cx & cy, np.uint8)
+
+    def run(s):
+        ti = part.train(s)
+        a = [np.ascontiguousarray(arr[ti], np.float64) for arr in (x, y, v)]
+        Xs = np.ascontiguousarray(X[ti])
+        cm = core_mask(s, ti)
+        A = np.zeros(p * p)
+        b = np.zeros(p)
+        rc = lib.oracle_gls_subset(ti.size, _ptr(a[0]), _ptr(a[1]), _ptr(a[2]), _ptr(Xs), _ptr(cm), p,
+                                   float(param[0]), float(param[1]), float(param[2]), _ptr(A), _ptr(b))
+        if rc:
+            raise OracleError(rc, "gls_subset")
+        As[s] = A.reshape(p, p)
+        bs[s] = b
+
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        list(ex.map(run, [int(s) for s in sub]))
+    A = np.zeros((p, p))
+    b = np.zeros(p)
+    for s in sub:  # ascending subset order
+        A = A + As[s]
+        b = b + bs[s]
+    beta = np.zeros(p)
+    Ac, bc = np.ascontiguousarray(A), np.ascontiguousarray(b)
+    rc = lib.oracle_solve_small(p, _ptr(Ac), _ptr(bc), _ptr(beta))
+    if rc:
+        raise OracleError(rc, "solve_small")
+    return beta, A, b

@@ -427,36 +427,144 @@ uint64_t oracle_splitmix64(uint64_t seed, uint64_t i) {
 
 /* Shell cap (shells with more than 2,000 residuals are reduced "to 2,000 by
  * random sampling"; reading R22): of subset s's training list (ascending p) the shell
- * members -- those outside the core rect -- are kept only if their key
- * splitmix64(seed, s * 2^32 + p + 1) is among the `cap` smallest (ties: smaller p);
- * core members are always kept.  Writes the kept list (ascending p) to out, its length
- * to *k_out. */
+ * members -- those outside the core rect -- are sorted by (key, p) with
+ * key = splitmix64(seed, s * 2^32 + p + 1) and only the first `cap` are kept; core members
+ * are always kept.  Writes the kept list (ascending p) to out, its length to *k_out. */
+typedef struct { uint64_t key; int32_t p; } keyed_t;
+static int cmp_keyed(const void *a, const void *b) {
+    const keyed_t *u = (const keyed_t *)a, *v = (const keyed_t *)b;
+    if (u->key != v->key) return u->key < v->key ? -1 : 1;
+    return (u->p > v->p) - (u->p < v->p);
+}
 int oracle_cap_shell(int64_t k, const int32_t *idx, const double *x, const double *y, const double *rect,
                      double xmax, double ymax, int64_t cap, uint64_t seed, int64_t s, int32_t *out,
                      int64_t *k_out) {
+    keyed_t *sh = malloc(sizeof(keyed_t) * (size_t)(k > 0 ? k : 1));
+    uint8_t *keep = malloc((size_t)(k > 0 ? k : 1));
+    if (!sh || !keep) { free(sh); free(keep); return OR_ENOMEM; }
     int64_t nshell = 0;
     for (int64_t i = 0; i < k; ++i) {
         int32_t p = idx[i];
-        if (!(in_core(x[p], rect[0], rect[1], xmax) && in_core(y[p], rect[2], rect[3], ymax))) ++nshell;
-    }
-    for (int64_t i = 0, o = 0; i < k; ++i) {
-        int32_t p = idx[i];
-        int keep = 1;
-        if (nshell > cap && !(in_core(x[p], rect[0], rect[1], xmax) && in_core(y[p], rect[2], rect[3], ymax))) {
-            /* rank of p among the shell members by (key, p): keep iff rank < cap */
-            uint64_t kp = oracle_splitmix64(seed, ((uint64_t)s << 32) + (uint64_t)p + 1);
-            int64_t rank = 0;
-            for (int64_t j = 0; j < k; ++j) {
-                int32_t q = idx[j];
-                if (in_core(x[q], rect[0], rect[1], xmax) && in_core(y[q], rect[2], rect[3], ymax)) continue;
-                uint64_t kq = oracle_splitmix64(seed, ((uint64_t)s << 32) + (uint64_t)q + 1);
-                if (kq < kp || (kq == kp && q < p)) ++rank;
-            }
-            keep = rank < cap;
+        int core = in_core(x[p], rect[0], rect[1], xmax) && in_core(y[p], rect[2], rect[3], ymax);
+        keep[i] = 1;
+        if (!core) {
+            sh[nshell].key = oracle_splitmix64(seed, ((uint64_t)s << 32) + (uint64_t)p + 1);
+            sh[nshell].p = p;
+            ++nshell;
         }
-        if (keep) out[o++] = p;
-        if (i == k - 1) *k_out = o;
     }
-    if (k == 0) *k_out = 0;
+    if (nshell > cap) {
+        qsort(sh, (size_t)nshell, sizeof(keyed_t), cmp_keyed);
+        /* drop the shell members of rank >= cap (lists are ascending in p: find by scan) */
+        for (int64_t r = cap; r < nshell; ++r)
+            for (int64_t i = 0; i < k; ++i)
+                if (idx[i] == sh[r].p) { keep[i] = 0; break; }
+    }
+    int64_t o = 0;
+    for (int64_t i = 0; i < k; ++i)
+        if (keep[i]) out[o++] = idx[i];
+    *k_out = o;
+    free(sh); free(keep);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Row f4: GLS mean estimation (Conclusion, Eq. GLS):
+ *   beta_hat = (X^T M^{-1} X)^{-1} X^T M^{-1} y,  M = Sigma + lambda I.
+ * The paper computes M^{-1} X "by a spatial prediction operation on the columns of X"
+ * (M^{-1} = (1/lambda)(I - H)).  Parallel reading (R23): as the CV
+ * loss replaces the global prediction by subset predictions, the rows of M^{-1} X and
+ * M^{-1} y at a training point p are taken from the system of the subset whose CORE holds
+ * p, (M^{-1} X)_p ~ (M_s^{-1} X^s)_p; every training point lies in exactly one core, so
+ *   X^T M^{-1} X ~ sum_s sum_{p in core_s} X_p^T (M_s^{-1} X^s)_p,  likewise X^T M^{-1} y,
+ * exact when one subset holds all data.  This function returns one subset's two partial
+ * sums, computed as written: form M_s, Cholesky, solve M_s W = [y | X] column by column
+ * (forward then backward substitution), accumulate over the core rows in ascending order.
+ *   Xs: k x p row-major covariates of the subset's training points; core[i] = 1 if
+ *   training point i lies in the subset's core.  out_A: p x p row-major,
+ *   A[a][b] = sum_core X[i][a] W_b[i];  out_b: p, b[a] = sum_core X[i][a] W_y[i].
+ * ------------------------------------------------------------------------- */
+int oracle_gls_subset(int64_t k, const double *tx, const double *ty, const double *tv, const double *Xs,
+                      const uint8_t *core, int32_t p, double range, double sigma2, double nugget,
+                      double *out_A, double *out_b) {
+    if (!(range > 0) || !(sigma2 > 0) || !(nugget >= 0) || p < 1) return OR_EINVAL;
+    for (int32_t a = 0; a < p; ++a) {
+        out_b[a] = 0.0;
+        for (int32_t b = 0; b < p; ++b) out_A[a * p + b] = 0.0;
+    }
+    if (k == 0) return OR_OK;
+    double lambda = nugget / sigma2;
+    double *L = malloc(sizeof(double) * (size_t)k * (size_t)k);
+    double *z = malloc(sizeof(double) * (size_t)k);
+    double *w = malloc(sizeof(double) * (size_t)k);
+    if (!L || !z || !w) { free(L); free(z); free(w); return OR_ENOMEM; }
+    for (int64_t i = 0; i < k; ++i) {
+        for (int64_t j = 0; j < i; ++j) {
+            double dx = tx[i] - tx[j], dy = ty[i] - ty[j];
+            L[i * k + j] = exp(-sqrt(dx * dx + dy * dy) / range);
+        }
+        L[i * k + i] = 1.0 + lambda;
+    }
+    for (int64_t i = 0; i < k; ++i)
+        for (int64_t j = 0; j <= i; ++j) {
+            double s = L[i * k + j];
+            for (int64_t q = 0; q < j; ++q) s -= L[i * k + q] * L[j * k + q];
+            if (i == j) {
+                if (!(s > 0)) { free(L); free(z); free(w); return OR_ENUMERIC; }
+                L[i * k + i] = sqrt(s);
+            } else {
+                L[i * k + j] = s / L[j * k + j];
+            }
+        }
+    for (int32_t col = -1; col < p; ++col) { /* col -1: y, else X column col */
+        for (int64_t i = 0; i < k; ++i) {
+            double s = col < 0 ? tv[i] : Xs[i * p + col];
+            for (int64_t q = 0; q < i; ++q) s -= L[i * k + q] * z[q];
+            z[i] = s / L[i * k + i];
+        }
+        for (int64_t i = k - 1; i >= 0; --i) {
+            double s = z[i];
+            for (int64_t q = i + 1; q < k; ++q) s -= L[q * k + i] * w[q];
+            w[i] = s / L[i * k + i];
+        }
+        for (int64_t i = 0; i < k; ++i) {
+            if (!core[i]) continue;
+            for (int32_t a = 0; a < p; ++a) {
+                if (col < 0) out_b[a] += Xs[i * p + a] * w[i];
+                else out_A[a * p + col] += Xs[i * p + a] * w[i];
+            }
+        }
+    }
+    free(L); free(z); free(w);
+    return OR_OK;
+}
+
+/* Solve A beta = b (p x p, row-major) by Gaussian elimination with partial pivoting
+ * (largest |pivot|, first on ties).  A singular pivot (exactly 0) gives OR_ENUMERIC. */
+int oracle_solve_small(int32_t p, const double *A_in, const double *b_in, double *beta) {
+    double A[64 * 64], b[64];
+    if (p < 1 || p > 64) return OR_EINVAL;
+    for (int32_t i = 0; i < p * p; ++i) A[i] = A_in[i];
+    for (int32_t i = 0; i < p; ++i) b[i] = b_in[i];
+    for (int32_t c = 0; c < p; ++c) {
+        int32_t piv = c;
+        for (int32_t r = c + 1; r < p; ++r)
+            if (fabs(A[r * p + c]) > fabs(A[piv * p + c])) piv = r;
+        if (A[piv * p + c] == 0.0) return OR_ENUMERIC;
+        if (piv != c) {
+            for (int32_t j = 0; j < p; ++j) { double t = A[c * p + j]; A[c * p + j] = A[piv * p + j]; A[piv * p + j] = t; }
+            double t = b[c]; b[c] = b[piv]; b[piv] = t;
+        }
+        for (int32_t r = c + 1; r < p; ++r) {
+            double f = A[r * p + c] / A[c * p + c];
+            for (int32_t j = c; j < p; ++j) A[r * p + j] -= f * A[c * p + j];
+            b[r] -= f * b[c];
+        }
+    }
+    for (int32_t r = p - 1; r >= 0; --r) {
+        double s = b[r];
+        for (int32_t j = r + 1; j < p; ++j) s -= A[r * p + j] * beta[j];
+        beta[r] = s / A[r * p + r];
+    }
     return OR_OK;
 }

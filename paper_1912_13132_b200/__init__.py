@@ -30,11 +30,12 @@ MAX_K = 19200
 # Symbols include/pgpcv.h declares (checked by tests/test_abi.py).
 EXPORTED = ("pgpcv_version", "pgpcv_create", "pgpcv_destroy", "pgpcv_last_error",
             "pgpcv_set_stream", "pgpcv_partition", "pgpcv_partition_device",
+            "pgpcv_partition_bisect", "pgpcv_partition_bisect_device", "pgpcv_partition_rects",
             "pgpcv_partition_export", "pgpcv_shard", "pgpcv_nccl_get_unique_id",
             "pgpcv_cv_loss", "pgpcv_evaluate", "pgpcv_select", "pgpcv_predict",
             "pgpcv_partition_export_test", "pgpcv_last_timing", "pgpcv_lpt_assign")
 ROLE_TRAIN, ROLE_VALIDATION, ROLE_TEST = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class PgpcvError(RuntimeError):
@@ -97,6 +98,10 @@ def load_library():
     lib.pgpcv_set_stream.argtypes = [p, p]
     lib.pgpcv_partition.argtypes = [p, i64, p, p, p, p, Rect, i32, i32, d, ctypes.POINTER(PartitionInfo)]
     lib.pgpcv_partition_device.argtypes = lib.pgpcv_partition.argtypes
+    lib.pgpcv_partition_bisect.argtypes = [p, i64, p, p, p, p, Rect, i32, d, i64, ctypes.c_uint64,
+                                           ctypes.POINTER(PartitionInfo)]
+    lib.pgpcv_partition_bisect_device.argtypes = lib.pgpcv_partition_bisect.argtypes
+    lib.pgpcv_partition_rects.argtypes = [p, p]
     lib.pgpcv_partition_export.argtypes = [p, p, p, p, p]
     lib.pgpcv_shard.argtypes = [p, ctypes.c_int, ctypes.c_int, p]
     lib.pgpcv_nccl_get_unique_id.argtypes = [p]
@@ -230,6 +235,47 @@ class Context:
         self._check(rc, "pgpcv_partition_device")
         self.info = info.as_dict()
         return self.info
+
+    def partition_bisect(self, x, y, value, role, domain, depth: int, delta: float, shell_cap: int = -1,
+                         seed: int = 0) -> dict:
+        """pgpcv_partition_bisect with host arrays (row f2: recursive shell-balanced bisection
+        into 2^depth subsets, optional shell cap)."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        v = np.ascontiguousarray(value, np.float64)
+        r = np.ascontiguousarray(role, np.uint8)
+        n = x.shape[0]
+        if not (y.shape[0] == v.shape[0] == r.shape[0] == n):
+            raise ValueError("x, y, value, role must have equal length")
+        info = PartitionInfo()
+        rc = self._lib.pgpcv_partition_bisect(self._h, n, _ptr(x), _ptr(y), _ptr(v), _ptr(r), Rect(*domain),
+                                              int(depth), float(delta), int(shell_cap), int(seed) & (2**64 - 1),
+                                              ctypes.byref(info))
+        self._check(rc, "pgpcv_partition_bisect")
+        self.info = info.as_dict()
+        return self.info
+
+    def partition_bisect_device(self, x, y, value, role, domain, depth: int, delta: float, shell_cap: int = -1,
+                                seed: int = 0) -> dict:
+        """pgpcv_partition_bisect_device: CUDA tensors on this context's device."""
+        def dp(t):
+            return ctypes.c_void_p(t if isinstance(t, int) else t.data_ptr())
+        n = x.numel() if hasattr(x, "numel") else int(len(x))
+        info = PartitionInfo()
+        rc = self._lib.pgpcv_partition_bisect_device(self._h, n, dp(x), dp(y), dp(value), dp(role), Rect(*domain),
+                                                     int(depth), float(delta), int(shell_cap),
+                                                     int(seed) & (2**64 - 1), ctypes.byref(info))
+        self._check(rc, "pgpcv_partition_bisect_device")
+        self.info = info.as_dict()
+        return self.info
+
+    def partition_rects(self) -> np.ndarray:
+        """pgpcv_partition_rects: [N, 4] (x0, x1, y0, y1) per subset."""
+        if self.info is None:
+            raise PgpcvError(ESTATE, "no partition")
+        out = np.empty((self.info["n_subsets"], 4), np.float64)
+        self._check(self._lib.pgpcv_partition_rects(self._h, _ptr(out)), "pgpcv_partition_rects")
+        return out
 
     def partition_export(self):
         """(train_off, train_idx, val_off, val_idx) CSR membership of the partition."""

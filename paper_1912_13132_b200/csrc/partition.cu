@@ -66,50 +66,48 @@ __global__ void validate_kernel(int64_t n, const double *x, const double *y, con
     if (nv) atomicAdd(stats + 2, nv);
 }
 
-__global__ void count_kernel(int64_t n, const double *x, const double *y, const uint8_t *role,
-                             Axis ax, Axis ay, unsigned int *train_cnt, unsigned int *val_cnt,
-                             unsigned int *test_cnt) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const uint8_t r = role[p];
-        const double px = x[p], py = y[p];
+// Visit the memberships of point (px, py) with role r under geometry g:
+//   r == 0: every subset whose dilated tile/rectangle holds the point (training, y~^s_T)
+//   r == 1 / 2: the core tile/rectangle (validation y^s_V / test targets)
+template <class F>
+__device__ __forceinline__ void for_each_member(const Geom &g, double px, double py, uint8_t r, F f) {
+    if (g.kind == 0) {
         if (r == 1 || r == 2) {
-            const int ix = core_index(px, ax.e, ax.K), iy = core_index(py, ay.e, ay.K);
-            atomicAdd((r == 1 ? val_cnt : test_cnt) + (int64_t)iy * ax.K + ix, 1u);
+            const int ix = core_index(px, g.ax.e, g.ax.K), iy = core_index(py, g.ay.e, g.ay.K);
+            f((int64_t)iy * g.ax.K + ix);
         } else if (r == 0) {
-            const int2 rx = dilated_range(px, ax), ry = dilated_range(py, ay);
+            const int2 rx = dilated_range(px, g.ax), ry = dilated_range(py, g.ay);
             for (int iy = ry.x; iy <= ry.y; ++iy)
-                for (int ix = rx.x; ix <= rx.y; ++ix)
-                    atomicAdd(train_cnt + (int64_t)iy * ax.K + ix, 1u);
+                for (int ix = rx.x; ix <= rx.y; ++ix) f((int64_t)iy * g.ax.K + ix);
         }
+    } else if (r <= 2) {
+        tree_visit(g.tree, px, py, [&](int s, bool, bool core) {
+            if (r == 0 || core) f((int64_t)s);
+        });
     }
 }
 
-__global__ void scatter_kernel(int64_t n, const double *x, const double *y, const uint8_t *role,
-                               Axis ax, Axis ay, const int64_t *train_off, const int64_t *val_off,
-                               const int64_t *test_off, unsigned int *train_cur, unsigned int *val_cur,
-                               unsigned int *test_cur, int32_t *train_idx, int32_t *val_idx,
-                               int32_t *test_idx) {
+__global__ void count_kernel(int64_t n, const double *x, const double *y, const uint8_t *role, Geom g,
+                             unsigned int *train_cnt, unsigned int *val_cnt, unsigned int *test_cnt) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         const uint8_t r = role[p];
-        const double px = x[p], py = y[p];
-        if (r == 1) {
-            const int ix = core_index(px, ax.e, ax.K), iy = core_index(py, ay.e, ay.K);
-            const int64_t s = (int64_t)iy * ax.K + ix;
-            val_idx[val_off[s] + atomicAdd(val_cur + s, 1u)] = (int32_t)p;
-        } else if (r == 2) {  // test points: core tile only, targets of pgpcv_predict
-            const int ix = core_index(px, ax.e, ax.K), iy = core_index(py, ay.e, ay.K);
-            const int64_t s = (int64_t)iy * ax.K + ix;
-            test_idx[test_off[s] + atomicAdd(test_cur + s, 1u)] = (int32_t)p;
-        } else if (r == 0) {
-            const int2 rx = dilated_range(px, ax), ry = dilated_range(py, ay);
-            for (int iy = ry.x; iy <= ry.y; ++iy)
-                for (int ix = rx.x; ix <= rx.y; ++ix) {
-                    const int64_t s = (int64_t)iy * ax.K + ix;
-                    train_idx[train_off[s] + atomicAdd(train_cur + s, 1u)] = (int32_t)p;
-                }
-        }
+        unsigned int *cnt = r == 0 ? train_cnt : r == 1 ? val_cnt : test_cnt;
+        for_each_member(g, x[p], y[p], r, [&](int64_t s) { atomicAdd(cnt + s, 1u); });
+    }
+}
+
+__global__ void scatter_kernel(int64_t n, const double *x, const double *y, const uint8_t *role, Geom g,
+                               const int64_t *train_off, const int64_t *val_off, const int64_t *test_off,
+                               unsigned int *train_cur, unsigned int *val_cur, unsigned int *test_cur,
+                               int32_t *train_idx, int32_t *val_idx, int32_t *test_idx) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t r = role[p];
+        const int64_t *off = r == 0 ? train_off : r == 1 ? val_off : test_off;
+        unsigned int *cur = r == 0 ? train_cur : r == 1 ? val_cur : test_cur;
+        int32_t *idx = r == 0 ? train_idx : r == 1 ? val_idx : test_idx;
+        for_each_member(g, x[p], y[p], r, [&](int64_t s) { idx[off[s] + atomicAdd(cur + s, 1u)] = (int32_t)p; });
     }
 }
 
@@ -233,10 +231,10 @@ cudaError_t launch_validate(int64_t n, const double *x, const double *y, const d
 }
 
 cudaError_t launch_count(int64_t n, const double *x, const double *y, const uint8_t *role,
-                         Axis ax, Axis ay, unsigned int *train_cnt, unsigned int *val_cnt,
+                         const Geom &g, unsigned int *train_cnt, unsigned int *val_cnt,
                          unsigned int *test_cnt, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    count_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, ax, ay, train_cnt, val_cnt, test_cnt);
+    count_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, g, train_cnt, val_cnt, test_cnt);
     return cudaGetLastError();
 }
 
@@ -246,12 +244,12 @@ cudaError_t launch_scan(const unsigned int *cnt, int64_t N, int64_t *off, cudaSt
 }
 
 cudaError_t launch_scatter(int64_t n, const double *x, const double *y, const uint8_t *role,
-                           Axis ax, Axis ay, const int64_t *train_off, const int64_t *val_off,
+                           const Geom &g, const int64_t *train_off, const int64_t *val_off,
                            const int64_t *test_off, unsigned int *train_cur, unsigned int *val_cur,
                            unsigned int *test_cur, int32_t *train_idx, int32_t *val_idx,
                            int32_t *test_idx, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, ax, ay, train_off, val_off, test_off,
+    scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, x, y, role, g, train_off, val_off, test_off,
                                                 train_cur, val_cur, test_cur, train_idx, val_idx,
                                                 test_idx);
     return cudaGetLastError();

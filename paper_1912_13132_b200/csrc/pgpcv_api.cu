@@ -26,7 +26,14 @@ template <typename T>
 struct DevBuf {
     T *p = nullptr;
     size_t cap = 0;  // elements
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() { release(); }
+    void swap(DevBuf &o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
+    }
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
@@ -130,10 +137,13 @@ struct pgpcv_ctx {
     // partition state
     bool has_partition = false;
     int64_t n = 0, N = 0;
-    int32_t kx = 0, ky = 0;
     DevBuf<double> px, py, pv;
     DevBuf<uint8_t> prole;
     DevBuf<double> bounds;  // ex, lox, hix, ey, loy, hiy
+    DevBuf<double> rects, split;      // subset rectangles [N*4]; bisection split per node id
+    std::vector<double> h_rects;
+    DevBuf<int64_t> train_off2;       // shell-cap output (swapped in)
+    DevBuf<int32_t> train_idx2;
     DevBuf<unsigned int> cnt, cur;
     DevBuf<unsigned long long> stats;
     DevBuf<int64_t> train_off, val_off, test_off;
@@ -207,10 +217,19 @@ void assign_owned(pgpcv_ctx *ctx) {
     for (int64_t s = 0; s < ctx->N; ++s) ctx->owned[s] = owner[s] == ctx->rank;
 }
 
+// How the subsets are formed: equal tiles (R1) or the recursive bisection (row f2).
+struct PartSpec {
+    int kind = 0;  // 0 grid, 1 bisection
+    int32_t kx = 1, ky = 1, depth = 0;
+    double delta = 0;
+    int64_t shell_cap = -1;  // < 0: no cap
+    uint64_t seed = 0;
+};
+
 int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, const double *v,
-                   const uint8_t *role, pgpcv_rect d, int32_t kx, int32_t ky, double delta,
-                   pgpcv_partition_info *info_out) {
+                   const uint8_t *role, pgpcv_rect d, const PartSpec &ps, pgpcv_partition_info *info_out) {
     cudaStream_t st = ctx->stream;
+    const double delta = ps.delta;
     ctx->has_partition = false;
     // K0: input validation on the device (NaN/Inf, outside D, bad role)
     CK(ctx->stats.ensure(3), "alloc stats");
@@ -225,25 +244,52 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     if (flags & 2u) return ctx->fail_with(PGPCV_EINVAL, "a point lies outside the domain");
     if (flags & 4u) return ctx->fail_with(PGPCV_EINVAL, "role byte not in {0,1,2}");
 
-    std::vector<double> ex, lox, hix, ey, loy, hiy;
-    if (!axis_bounds(d.xmin, d.xmax, kx, delta, ex, lox, hix) ||
-        !axis_bounds(d.ymin, d.ymax, ky, delta, ey, loy, hiy))
-        return ctx->fail_with(PGPCV_EINVAL, "tile edges are not strictly increasing");
-    std::vector<double> hb;
-    for (auto *vec : {&ex, &lox, &hix, &ey, &loy, &hiy}) hb.insert(hb.end(), vec->begin(), vec->end());
-    CK(ctx->bounds.ensure(hb.size()), "alloc bounds");
-    CK(cudaMemcpyAsync(ctx->bounds.p, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice, st),
-       "copy bounds");
-    double *b = ctx->bounds.p;
-    Axis ax{b, b + (kx + 1), b + (kx + 1) + kx, kx};
-    double *b2 = b + (kx + 1) + 2 * kx;
-    Axis ay{b2, b2 + (ky + 1), b2 + (ky + 1) + ky, ky};
-
-    const int64_t N = (int64_t)kx * ky;
+    Geom geom{};
+    int64_t N = 0;
+    if (ps.kind == 0) {
+        const int32_t kx = ps.kx, ky = ps.ky;
+        std::vector<double> ex, lox, hix, ey, loy, hiy;
+        if (!axis_bounds(d.xmin, d.xmax, kx, delta, ex, lox, hix) ||
+            !axis_bounds(d.ymin, d.ymax, ky, delta, ey, loy, hiy))
+            return ctx->fail_with(PGPCV_EINVAL, "tile edges are not strictly increasing");
+        std::vector<double> hb;
+        for (auto *vec : {&ex, &lox, &hix, &ey, &loy, &hiy}) hb.insert(hb.end(), vec->begin(), vec->end());
+        CK(ctx->bounds.ensure(hb.size()), "alloc bounds");
+        CK(cudaMemcpyAsync(ctx->bounds.p, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice, st),
+           "copy bounds");
+        double *b = ctx->bounds.p;
+        double *b2 = b + (kx + 1) + 2 * kx;
+        geom.kind = 0;
+        geom.ax = Axis{b, b + (kx + 1), b + (kx + 1) + kx, kx};
+        geom.ay = Axis{b2, b2 + (ky + 1), b2 + (ky + 1) + ky, ky};
+        N = (int64_t)kx * ky;
+        ctx->h_rects.resize(4 * N);  // tile s = iy*kx + ix is [e_ix, e_ix+1) x [e_iy, e_iy+1)
+        for (int32_t iy = 0; iy < ky; ++iy)
+            for (int32_t ix = 0; ix < kx; ++ix) {
+                double *r = &ctx->h_rects[4 * ((int64_t)iy * kx + ix)];
+                r[0] = ex[ix];
+                r[1] = ex[ix + 1];
+                r[2] = ey[iy];
+                r[3] = ey[iy + 1];
+            }
+        CK(ctx->rects.ensure(4 * N), "alloc rects");
+        CK(cudaMemcpyAsync(ctx->rects.p, ctx->h_rects.data(), sizeof(double) * 4 * N, cudaMemcpyHostToDevice, st),
+           "copy rects");
+    } else {
+        // row f2: the tree, level by level on the device (bisect.cu)
+        N = (int64_t)1 << ps.depth;
+        CK(ctx->split.ensure(N), "alloc split");
+        CK(ctx->rects.ensure(4 * N), "alloc rects");
+        CK(bisect_tree(n, x, y, role, d.xmin, d.xmax, d.ymin, d.ymax, ps.depth, delta, ctx->split.p, ctx->rects.p,
+                       st), "bisection");
+        geom.kind = 1;
+        geom.tree = Tree{ctx->split.p, ctx->rects.p, ps.depth, d.xmax, d.ymax, delta};
+        ctx->h_rects.resize(4 * N);
+        CK(cudaMemcpyAsync(ctx->h_rects.data(), ctx->rects.p, sizeof(double) * 4 * N, cudaMemcpyDeviceToHost, st),
+           "copy rects");
+    }
     ctx->N = N;
     ctx->n = n;
-    ctx->kx = kx;
-    ctx->ky = ky;
     // K1 count, K2 scan
     CK(ctx->cnt.ensure(3 * N), "alloc counts");
     CK(ctx->cur.ensure(3 * N), "alloc cursors");
@@ -251,7 +297,7 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     CK(ctx->val_off.ensure(N + 1), "alloc offsets");
     CK(ctx->test_off.ensure(N + 1), "alloc offsets");
     CK(cudaMemsetAsync(ctx->cnt.p, 0, sizeof(unsigned) * 3 * N, st), "memset");
-    CK(launch_count(n, x, y, role, ax, ay, ctx->cnt.p, ctx->cnt.p + N, ctx->cnt.p + 2 * N, st),
+    CK(launch_count(n, x, y, role, geom, ctx->cnt.p, ctx->cnt.p + N, ctx->cnt.p + 2 * N, st),
        "count kernel");
     CK(launch_scan(ctx->cnt.p, N, ctx->train_off.p, st), "scan kernel");
     CK(launch_scan(ctx->cnt.p + N, N, ctx->val_off.p, st), "scan kernel");
@@ -274,7 +320,7 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     CK(ctx->val_idx.ensure(sum_m), "alloc val_idx");
     CK(ctx->test_idx.ensure(sum_g), "alloc test_idx");
     CK(cudaMemsetAsync(ctx->cur.p, 0, sizeof(unsigned) * 3 * N, st), "memset");
-    CK(launch_scatter(n, x, y, role, ax, ay, ctx->train_off.p, ctx->val_off.p, ctx->test_off.p,
+    CK(launch_scatter(n, x, y, role, geom, ctx->train_off.p, ctx->val_off.p, ctx->test_off.p,
                       ctx->cur.p, ctx->cur.p + N, ctx->cur.p + 2 * N, ctx->train_idx.p,
                       ctx->val_idx.p, ctx->test_idx.p, st), "scatter kernel");
     int64_t max_k = 0, max_m = 0, max_g = 0, empty = 0;
@@ -299,24 +345,40 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
             }
         }
     }
+    // row f2: shell cap (R22) on the sorted training lists
+    int64_t dropped = 0;
+    if (ps.shell_cap >= 0) {
+        CK(ctx->train_idx2.ensure(std::max<int64_t>(sum_k, 1)), "alloc");
+        CK(ctx->train_off2.ensure(N + 1), "alloc");
+        CK(cap_shells(N, ctx->train_off.p, ctx->train_idx.p, x, y, ctx->rects.p, d.xmax, d.ymax, ps.shell_cap,
+                      ps.seed, ctx->train_idx2.p, ctx->train_off2.p, &dropped, st), "shell cap");
+        ctx->train_idx.swap(ctx->train_idx2);
+        ctx->train_off.swap(ctx->train_off2);
+        CK(cudaMemcpyAsync(ctx->h_train_off.data(), ctx->train_off.p, sizeof(int64_t) * (N + 1),
+                           cudaMemcpyDeviceToHost, st), "copy offsets");
+        CK(cudaStreamSynchronize(st), "shell cap");
+        max_k = 0;
+        for (int64_t s = 0; s < N; ++s) max_k = std::max(max_k, ctx->h_train_off[s + 1] - ctx->h_train_off[s]);
+    }
+    const int64_t sum_k_final = sum_k - dropped;
     // K4 staging gather (subset-contiguous SoA)
-    CK(ctx->tx.ensure(sum_k), "alloc");
-    CK(ctx->ty.ensure(sum_k), "alloc");
-    CK(ctx->tv.ensure(sum_k), "alloc");
+    CK(ctx->tx.ensure(sum_k_final), "alloc");
+    CK(ctx->ty.ensure(sum_k_final), "alloc");
+    CK(ctx->tv.ensure(sum_k_final), "alloc");
     CK(ctx->vx.ensure(sum_m), "alloc");
     CK(ctx->vy.ensure(sum_m), "alloc");
     CK(ctx->vv.ensure(sum_m), "alloc");
     CK(ctx->gx.ensure(sum_g), "alloc");
     CK(ctx->gy.ensure(sum_g), "alloc");
     CK(ctx->gv.ensure(sum_g), "alloc");
-    CK(launch_gather(sum_k, ctx->train_idx.p, x, y, v, ctx->tx.p, ctx->ty.p, ctx->tv.p, st), "gather");
+    CK(launch_gather(sum_k_final, ctx->train_idx.p, x, y, v, ctx->tx.p, ctx->ty.p, ctx->tv.p, st), "gather");
     CK(launch_gather(sum_m, ctx->val_idx.p, x, y, v, ctx->vx.p, ctx->vy.p, ctx->vv.p, st), "gather");
     CK(launch_gather(sum_g, ctx->test_idx.p, x, y, v, ctx->gx.p, ctx->gy.p, ctx->gv.p, st), "gather");
     CK(cudaStreamSynchronize(st), "partition");
 
     pgpcv_partition_info &info = ctx->info;
     info.n_subsets = N;
-    info.sum_k = sum_k;
+    info.sum_k = sum_k_final;
     info.sum_m = sum_m;
     info.max_k = max_k;
     info.max_m = max_m;
@@ -442,8 +504,11 @@ int pgpcv_partition(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y,
         CK(cudaMemcpyAsync(ctx->pv.p, value, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy v");
         CK(cudaMemcpyAsync(ctx->prole.p, role, n, cudaMemcpyHostToDevice, st), "copy role");
     }
-    return partition_impl(ctx, n, ctx->px.p, ctx->py.p, ctx->pv.p, ctx->prole.p, domain, kx, ky,
-                          delta, info_out);
+    PartSpec ps;
+    ps.kx = kx;
+    ps.ky = ky;
+    ps.delta = delta;
+    return partition_impl(ctx, n, ctx->px.p, ctx->py.p, ctx->pv.p, ctx->prole.p, domain, ps, info_out);
 }
 
 int pgpcv_partition_device(pgpcv_ctx *ctx, int64_t n, const double *d_x, const double *d_y,
@@ -453,7 +518,63 @@ int pgpcv_partition_device(pgpcv_ctx *ctx, int64_t n, const double *d_x, const d
     int rc = check_partition_args(ctx, n, d_x, d_y, d_value, d_role, domain, kx, ky, delta);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
-    return partition_impl(ctx, n, d_x, d_y, d_value, d_role, domain, kx, ky, delta, info_out);
+    PartSpec ps;
+    ps.kx = kx;
+    ps.ky = ky;
+    ps.delta = delta;
+    return partition_impl(ctx, n, d_x, d_y, d_value, d_role, domain, ps, info_out);
+}
+
+static int bisect_spec(pgpcv_ctx *ctx, int32_t depth, double delta, int64_t shell_cap, uint64_t seed, PartSpec &ps) {
+    if (depth < 0 || depth > 20) return ctx->fail_with(PGPCV_EINVAL, "depth must be in [0, 20]");
+    ps.kind = 1;
+    ps.depth = depth;
+    ps.delta = delta;
+    ps.shell_cap = shell_cap;
+    ps.seed = seed;
+    return PGPCV_OK;
+}
+
+int pgpcv_partition_bisect(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, const double *value,
+                           const uint8_t *role, pgpcv_rect domain, int32_t depth, double delta, int64_t shell_cap,
+                           uint64_t seed, pgpcv_partition_info *info_out) {
+    if (!ctx) return PGPCV_EINVAL;
+    int rc = check_partition_args(ctx, n, x, y, value, role, domain, 1, 1, delta);
+    if (rc) return rc;
+    PartSpec ps;
+    if ((rc = bisect_spec(ctx, depth, delta, shell_cap, seed, ps))) return rc;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    CK(ctx->px.ensure(n), "alloc points");
+    CK(ctx->py.ensure(n), "alloc points");
+    CK(ctx->pv.ensure(n), "alloc points");
+    CK(ctx->prole.ensure(n), "alloc points");
+    if (n > 0) {
+        CK(cudaMemcpyAsync(ctx->px.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy x");
+        CK(cudaMemcpyAsync(ctx->py.p, y, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy y");
+        CK(cudaMemcpyAsync(ctx->pv.p, value, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy v");
+        CK(cudaMemcpyAsync(ctx->prole.p, role, n, cudaMemcpyHostToDevice, st), "copy role");
+    }
+    return partition_impl(ctx, n, ctx->px.p, ctx->py.p, ctx->pv.p, ctx->prole.p, domain, ps, info_out);
+}
+
+int pgpcv_partition_bisect_device(pgpcv_ctx *ctx, int64_t n, const double *d_x, const double *d_y,
+                                  const double *d_value, const uint8_t *d_role, pgpcv_rect domain, int32_t depth,
+                                  double delta, int64_t shell_cap, uint64_t seed, pgpcv_partition_info *info_out) {
+    if (!ctx) return PGPCV_EINVAL;
+    int rc = check_partition_args(ctx, n, d_x, d_y, d_value, d_role, domain, 1, 1, delta);
+    if (rc) return rc;
+    PartSpec ps;
+    if ((rc = bisect_spec(ctx, depth, delta, shell_cap, seed, ps))) return rc;
+    cudaSetDevice(ctx->device);
+    return partition_impl(ctx, n, d_x, d_y, d_value, d_role, domain, ps, info_out);
+}
+
+int pgpcv_partition_rects(pgpcv_ctx *ctx, double *rects) {
+    if (!ctx || !rects) return PGPCV_EINVAL;
+    if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "no partition");
+    memcpy(rects, ctx->h_rects.data(), sizeof(double) * ctx->h_rects.size());
+    return PGPCV_OK;
 }
 
 int pgpcv_partition_export(pgpcv_ctx *ctx, int64_t *train_off, int32_t *train_idx, int64_t *val_off,

@@ -66,15 +66,71 @@ struct Axis {
     int32_t K;
 };
 
+// Bisection tree (row f2): internal node id (1 = D, children 2i / 2i+1) splits along x at
+// even depth and along y at odd depth at split[id]; rect[] holds the rectangles of the
+// 2^depth nodes at `depth` (the leaves), as (x0, x1, y0, y1), closed at the domain top.
+struct Tree {
+    const double *split;  // [2^depth] (entry 0 unused)
+    const double *rect;   // [2^depth * 4]
+    int32_t depth;
+    double xmax, ymax;
+    double delta;
+};
+
+// Membership geometry of a partition: equal tiles (R1) or the leaves of a bisection tree.
+struct Geom {
+    int32_t kind;  // 0 grid, 1 tree
+    Axis ax, ay;
+    Tree tree;
+};
+
+#ifdef __CUDACC__
+// R2/R3 dilated interval of [lo, hi): lo - delta <= u < hi + delta, hi = +inf at the top.
+__device__ __forceinline__ bool in_dilated_iv(double u, double lo, double hi, double top, double delta) {
+    const double l = __dsub_rn(lo, delta);
+    const double h = hi == top ? __longlong_as_double(0x7ff0000000000000ll) : __dadd_rn(hi, delta);
+    return l <= u && u < h;
+}
+// half-open core interval, closed at the domain top (R3)
+__device__ __forceinline__ bool in_core_iv(double u, double lo, double hi, double top) {
+    return lo <= u && (u < hi || (hi == top && u == top));
+}
+// f(leaf, in_dilated, in_core) for every leaf whose dilated rectangle contains (x, y).
+// Descent prunes with u < c + delta (left) and u >= c - delta (right), both implied by the
+// exact leaf test, so no member is lost; the leaf test itself decides.
+template <class F>
+__device__ __forceinline__ void tree_visit(const Tree &t, double x, double y, F f) {
+    int stack[48];
+    int sp = 0;
+    stack[sp++] = 1;
+    while (sp) {
+        const int id = stack[--sp];
+        const int dep = 31 - __clz(id);
+        if (dep == t.depth) {
+            const int s = id - (1 << t.depth);
+            const double *r = t.rect + 4 * s;
+            const bool dil = in_dilated_iv(x, r[0], r[1], t.xmax, t.delta) &&
+                             in_dilated_iv(y, r[2], r[3], t.ymax, t.delta);
+            if (dil) f(s, true, in_core_iv(x, r[0], r[1], t.xmax) && in_core_iv(y, r[2], r[3], t.ymax));
+            continue;
+        }
+        const double c = t.split[id];
+        const double u = (dep & 1) ? y : x;
+        if (u >= __dsub_rn(c, t.delta)) stack[sp++] = 2 * id + 1;
+        if (u < __dadd_rn(c, t.delta)) stack[sp++] = 2 * id;
+    }
+}
+#endif
+
 cudaError_t launch_validate(int64_t n, const double *x, const double *y, const double *v,
                             const uint8_t *role, double xmin, double xmax, double ymin,
                             double ymax, unsigned long long *stats, cudaStream_t st);
 cudaError_t launch_count(int64_t n, const double *x, const double *y, const uint8_t *role,
-                         Axis ax, Axis ay, unsigned int *train_cnt, unsigned int *val_cnt,
+                         const Geom &g, unsigned int *train_cnt, unsigned int *val_cnt,
                          unsigned int *test_cnt, cudaStream_t st);
 cudaError_t launch_scan(const unsigned int *cnt, int64_t N, int64_t *off, cudaStream_t st);
 cudaError_t launch_scatter(int64_t n, const double *x, const double *y, const uint8_t *role,
-                           Axis ax, Axis ay, const int64_t *train_off, const int64_t *val_off,
+                           const Geom &g, const int64_t *train_off, const int64_t *val_off,
                            const int64_t *test_off, unsigned int *train_cur, unsigned int *val_cur,
                            unsigned int *test_cur, int32_t *train_idx, int32_t *val_idx,
                            int32_t *test_idx, cudaStream_t st);
@@ -88,5 +144,22 @@ cudaError_t sort_long_segment(int32_t *idx, int64_t begin, int64_t len, int64_t 
 constexpr int64_t kSmallSortMax = 32768;
 cudaError_t launch_gather(int64_t cnt, const int32_t *idx, const double *x, const double *y,
                           const double *v, double *ox, double *oy, double *ov, cudaStream_t st);
+
+// ----------------------------------------------------------------------------------------
+// Recursive shell-balanced bisection (row f2; bisect.cu).
+// ----------------------------------------------------------------------------------------
+// Computes split[1 .. 2^depth - 1] and the leaf rectangles rect[2^depth * 4] (device
+// arrays, caller-allocated) for points with role <= 1, level by level; scratch comes from
+// the stream-ordered allocator.  Synchronises `st` once per level.
+cudaError_t bisect_tree(int64_t n, const double *x, const double *y, const uint8_t *role, double xmin,
+                        double xmax, double ymin, double ymax, int depth, double delta, double *split,
+                        double *rect, cudaStream_t st);
+// Shell cap (R22) on CSR training lists (ascending index) of N subsets with rectangles
+// rect (device arrays): writes the capped lists (ascending index) to train_idx_out /
+// train_off_out (device, capacity sum_k / N+1) and the number of dropped members to
+// *n_dropped (host).  Synchronises `st`.
+cudaError_t cap_shells(int64_t N, const int64_t *train_off, const int32_t *train_idx, const double *x,
+                       const double *y, const double *rect, double xmax, double ymax, int64_t cap, uint64_t seed,
+                       int32_t *train_idx_out, int64_t *train_off_out, int64_t *n_dropped, cudaStream_t st);
 
 }  // namespace pgpcv

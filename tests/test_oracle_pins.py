@@ -609,3 +609,70 @@ def test_shell_cap_rules():
         full, kept, core = set(part.train(s)), a.train(s), set(core_only.train(s))
         assert np.all(np.diff(kept) > 0) and set(kept) <= full and core <= set(kept)
         assert len(set(kept) - core) == min(len(full - core), cap)
+
+
+# ----------------------------------------------------------------- row f4: GLS
+
+def _gls_setup(seed, n, depth, delta):
+    x, y, v, role = workloads.random_points(seed, n, frac_val=0.1)
+    X = np.stack([np.ones(n), x - 0.5, (y - 0.5) ** 2], 1)
+    _, rects = oracle.bisect(x, y, role, (0, 1, 0, 1), depth, delta)
+    part = oracle.partition_rects(x, y, role, (0, 1, 0, 1), rects, delta)
+    return x, y, v, role, X, rects, part
+
+
+def test_gls_single_subset_is_dense_gls():
+    """One subset: the GLS estimate of Eq. GLS exactly, against a dense LAPACK
+    route (scipy cho_solve of M, numpy solve of the normal equations)."""
+    x, y, v, role, X, rects, part = _gls_setup(31, 400, 0, 0.0)
+    prm = (0.15, 1.3, 0.2)
+    beta, A, b = oracle.gls(x, y, v, X, part, rects, (0, 1, 0, 1), prm)
+    t = role == 0
+    M = _cov(x[t], y[t], x[t], y[t], prm[0]) + (prm[2] / prm[1]) * np.eye(int(t.sum()))
+    cf = scipy.linalg.cho_factor(M, lower=True)
+    MiX, Miy = scipy.linalg.cho_solve(cf, X[t]), scipy.linalg.cho_solve(cf, v[t])
+    np.testing.assert_allclose(A, X[t].T @ MiX, rtol=1e-10)
+    np.testing.assert_allclose(b, X[t].T @ Miy, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(beta, np.linalg.solve(X[t].T @ MiX, X[t].T @ Miy), rtol=1e-9)
+
+
+def test_gls_reproduces_exact_linear_mean_on_any_division():
+    """y = X beta0 exactly: A beta0 = b holds term by term for every subset division, so
+    beta_hat = beta0 whatever the subsets and shells (a property of reading R23)."""
+    x, y, v, role, X, rects, part = _gls_setup(32, 1500, 3, 0.1)
+    beta0 = np.array([0.7, -1.25, 2.0])
+    beta, _, _ = oracle.gls(x, y, X @ beta0, X, part, rects, (0, 1, 0, 1), (0.1, 1.0, 0.05))
+    np.testing.assert_allclose(beta, beta0, rtol=1e-9)
+
+
+def test_gls_large_nugget_is_ols_mean():
+    """X = 1 and lambda -> infinity: M ~ lambda I, the GLS estimate tends to mean(y_T)."""
+    x, y, v, role, X, rects, part = _gls_setup(33, 500, 2, 0.05)
+    beta, _, _ = oracle.gls(x, y, v, X[:, :1], part, rects, (0, 1, 0, 1), (0.1, 1.0, 1e9))
+    assert beta[0] == pytest.approx(v[role == 0].mean(), rel=1e-6)
+
+
+def test_gls_rows_match_the_papers_prediction_identity():
+    """M^{-1} = (1/lambda)(I - H), H = Sigma (Sigma + lambda I)^{-1} (P:522-524): the
+    subset GLS sums equal the ones built from the oracle's kriging predictions of the X
+    columns at the training sites (the paper's 'spatial prediction operation')."""
+    x, y, v, role, X, rects, part = _gls_setup(34, 300, 1, 0.1)
+    prm = (0.2, 1.0, 0.3)
+    lam = prm[2] / prm[1]
+    _, A, b = oracle.gls(x, y, v, X, part, rects, (0, 1, 0, 1), prm)
+    A2, b2 = np.zeros_like(A), np.zeros_like(b)
+    for s in range(2):
+        ti = part.train(s)
+        x0, x1, y0, y1 = rects[s]
+        core = (x0 <= x[ti]) & ((x[ti] < x1) | (x1 == 1.0)) & (y0 <= y[ti]) & ((y[ti] < y1) | (y1 == 1.0))
+        cols = []
+        for col in [v[ti]] + [X[ti, j] for j in range(X.shape[1])]:
+            # Eq.3 predicting the training sites themselves gives H col (the cross-covariance
+            # row of a training site is its Sigma row), so M^{-1} col = (col - H col) / lambda
+            _, pred = oracle.subset_cv(x[ti], y[ti], col, x[ti], y[ti], np.zeros(ti.size), *prm, return_yhat=True)
+            cols.append((col - pred) / lam)
+        Wy, WX = cols[0], np.stack(cols[1:], 1)
+        A2 += X[ti][core].T @ WX[core]
+        b2 += X[ti][core].T @ Wy[core]
+    np.testing.assert_allclose(A, A2, rtol=1e-8)
+    np.testing.assert_allclose(b, b2, rtol=1e-8, atol=1e-9)
