@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PGPCV_VERSION 3
+#define PGPCV_VERSION 4
 
 /* Error codes. */
 #define PGPCV_OK 0
@@ -273,6 +273,22 @@ int pgpcv_select(pgpcv_ctx *ctx, int32_t *best, double *rmspe, int32_t *local_be
 int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params,
                   const int32_t *subset_config, int32_t target_role, double *yhat,
                   double *subset_sspe, double *sspe);
+
+/* Row f4: GLS estimate of a linear mean (Conclusion, Eq. GLS)
+ *   beta_hat = (X^T M^{-1} X)^{-1} X^T M^{-1} y,  M = Sigma + lambda I,
+ * with M^{-1} X obtained "by a spatial prediction operation" per subset: the
+ * rows of M^{-1} [X | y] at a training point are those of the system of the subset whose
+ * core holds the point (R23) -- exact when one subset holds all data.  One
+ * factorization per subset serves all p + 1 right-hand sides (bordered rows).
+ *   X: host double[n * p], row-major per input point (the n points of the partition call,
+ *      in their order); only the training points' rows are used.  1 <= p <= 8.
+ *   param: one configuration (range, sigma2, nugget).
+ *   beta: host double[p] out.  xtmx: double[p*p] row-major or NULL; xtmy: double[p] or NULL
+ *      (the summed normal equations X^T M^{-1} X, X^T M^{-1} y).
+ * Errors: EINVAL, ESTATE, ENUMERIC (a non-PD subset -> NaN sums; or a singular p x p
+ * system -> beta NaN), ECUDA, ENOMEM, ENCCL. */
+int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, double *beta,
+              double *xtmx, double *xtmy);
 
 /* CSR lists of the test points (role 2) per core tile: test_off int64[N+1], test_idx
  * int32[n_test] (ascending point index within a subset).  Either may be NULL.

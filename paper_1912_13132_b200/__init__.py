@@ -33,9 +33,9 @@ EXPORTED = ("pgpcv_version", "pgpcv_create", "pgpcv_destroy", "pgpcv_last_error"
             "pgpcv_partition_bisect", "pgpcv_partition_bisect_device", "pgpcv_partition_rects",
             "pgpcv_partition_export", "pgpcv_shard", "pgpcv_nccl_get_unique_id",
             "pgpcv_cv_loss", "pgpcv_evaluate", "pgpcv_select", "pgpcv_predict",
-            "pgpcv_partition_export_test", "pgpcv_last_timing", "pgpcv_lpt_assign")
+            "pgpcv_partition_export_test", "pgpcv_gls", "pgpcv_last_timing", "pgpcv_lpt_assign")
 ROLE_TRAIN, ROLE_VALIDATION, ROLE_TEST = 0, 1, 2
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class PgpcvError(RuntimeError):
@@ -110,6 +110,7 @@ def load_library():
     lib.pgpcv_select.argtypes = [p, p, p, p, p, p]
     lib.pgpcv_predict.argtypes = [p, ctypes.POINTER(Param), i32, p, i32, p, p, p]
     lib.pgpcv_partition_export_test.argtypes = [p, p, p]
+    lib.pgpcv_gls.argtypes = [p, p, i32, Param, p, p, p]
     lib.pgpcv_last_timing.argtypes = [p, ctypes.POINTER(Timing)]
     lib.pgpcv_lpt_assign.argtypes = [i64, p, i32, p]
     for name in EXPORTED:
@@ -372,6 +373,24 @@ class Context:
         if rc not in (OK, ENUMERIC):
             self._check(rc, "pgpcv_predict")
         return Prediction(float(tot[0]), sub, yhat, rc)
+
+    def gls(self, X, param):
+        """pgpcv_gls (row f4): (beta, X^T M^-1 X, X^T M^-1 y) for covariates X [n, p] of the
+        partition's points and one (range, sigma2, nugget)."""
+        if self.info is None:
+            raise PgpcvError(ESTATE, "no partition")
+        X = np.ascontiguousarray(X, np.float64)
+        if X.ndim != 2:
+            raise ValueError("X must be [n, p]")
+        p = X.shape[1]
+        beta = np.empty(p)
+        A = np.empty((p, p))
+        b = np.empty(p)
+        rc = self._lib.pgpcv_gls(self._h, _ptr(X), p, Param(*[float(v) for v in param]), _ptr(beta), _ptr(A),
+                                 _ptr(b))
+        if rc not in (OK, ENUMERIC):
+            self._check(rc, "pgpcv_gls")
+        return beta, A, b
 
     def partition_export_test(self):
         """(test_off, test_idx): CSR lists of the test points (role 2) per core tile."""

@@ -41,6 +41,7 @@
 // cross-warp exchange.  110.7 KB of SMEM and <= 128
 // registers per thread let two CTAs share an SM, so one CTA's barriers, epilogue,
 // diagonal factorization and back-substitution overlap the other's DMMA stream.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -215,7 +216,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         const double nugget = a.params[3 * c + 2];
         const double lam = nugget / sigma2;
         const double ninv = -1.0 / range;
-        const int64_t ld = factor_ld(k);
+        const int np = (a.flags & kCvGls) ? a.p : 0;  // covariate rows bordered below y (f4)
+        const int kb = k + np;                          // last bordered row
+        const int64_t ld = factor_ld(kb);
         const int nblk = (k + NB - 1) / NB;
         const int64_t oi = (int64_t)s * a.out_C + (a.out_C > 1 ? c : 0);  // output entry
         bool failed = false;
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         for (int jb = 0; jb < nblk && !failed; ++jb) {
             const int j0 = jb * NB;
             const int jw = min(NB, k - j0);
-            const int nrows = k + 1 - j0;  // rows j0..k (row k: bordered y)
+            const int nrows = kb + 1 - j0;  // rows j0..kb (row k: bordered y, then covariates)
             const int ntiles = (nrows + MT - 1) / MT;
             const int nk = j0 / KC;        // operand chunks per tile
             for (int i = tid; i < NB; i += NT) {
@@ -266,8 +269,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 const int nl = j * 8 + 2 * t + e;
                                 const int cc = j0 + nl;
                                 double av;
-                                if (cc >= k || r > k) av = 0.0;
+                                if (cc >= k || r > kb) av = 0.0;
                                 else if (r == k) av = cv[nl];        // bordered row: y_T
+                                else if (r > k) av = __ldg(a.tX + (toff + cc) * np + (r - k - 1));
                                 else if (r == cc) av = 1.0 + lam;    // exp(0) + lambda
                                 else if (r < cc) av = 0.0;           // upper triangle: unused
                                 else {
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                             for (int e = 0; e < 2; ++e) {
                                 const int r = rbase + i * 8 + g;
                                 const int nl = h * 32 + j * 8 + 2 * t + e;
-                                if (nl < jw && r <= k && r >= rskip)
+                                if (nl < jw && r <= kb && r >= rskip)
                                     L[lidx(ld, r, j0 + nl)] = -xo[i][j][e];
                             }
                 }
@@ -483,7 +487,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             }
             __syncthreads();
         }
-        if (!(a.flags & kCvPredict) || m == 0) {
+        if (!(a.flags & (kCvPredict | kCvGls)) || ((a.flags & kCvPredict) && m == 0)) {
             if (tid == 0) {
                 if (a.flags & kCvPredict) a.subset_loss[oi] = 0.0;  // R10: no targets
                 a.fail[oi] = 0;
@@ -501,6 +505,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         double *part2 = alpha_smem ? stage + STAGE_DBL - NWARP * NB : stage;
         double *LB = Bt;        // diagonal block, [row][col] stride LJS
         double *tvec = cx;      // NB
+        // L^T alpha = (bordered row rrow): rrow = k gives alpha = (Sigma + lambda I)^{-1} y;
+        // rrow = k + 1 + q gives (Sigma + lambda I)^{-1} X[:, q] (GLS).
+        auto backsub = [&](int rrow) {
         for (int jb = nblk - 1; jb >= 0; --jb) {
             const int j0 = jb * NB;
             const int jw = min(NB, k - j0);
@@ -531,7 +538,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             if (tid < jw) {
                 double sum = 0.0;
                 for (int w = 0; w < NWARP; ++w) sum += part2[w * NB + tid];
-                tvec[tid] = __ldcg(L + lidx(ld, k, j0 + tid)) - sum;  // z_c - L[c+1:, c] . alpha
+                tvec[tid] = __ldcg(L + lidx(ld, rrow, j0 + tid)) - sum;  // z_c - L[c+1:, c] . alpha
             }
             __syncthreads();
             if (warp == 0) {
@@ -547,6 +554,48 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             }
             __syncthreads();
         }
+        };
+
+        if (a.flags & kCvGls) {
+            // ---------------- GLS normal-equation sums (Eq. GLS; R23) ----------
+            // W_q = (Sigma + lambda I)^{-1} [y | X]_q; over the training points in the
+            // subset's core: b[c] += X[i][c] W_y[i], A[c][q] += X[i][c] W_q[i].
+            const double *rc = a.rects + 4 * s;
+            const int W = (np + 1) * np;
+            for (int q = 0; q <= np; ++q) {
+                backsub(k + q);
+                double accq[kMaxCovariates];
+#pragma unroll
+                for (int cI = 0; cI < kMaxCovariates; ++cI) accq[cI] = 0.0;
+                for (int i = tid; i < k; i += NT) {
+                    if (!(in_core_iv(__ldg(tx + i), rc[0], rc[1], a.xmax) &&
+                          in_core_iv(__ldg(ty + i), rc[2], rc[3], a.ymax)))
+                        continue;
+                    const double wi = alpha[i];
+#pragma unroll
+                    for (int cI = 0; cI < kMaxCovariates; ++cI)
+                        if (cI < np) accq[cI] += __ldg(a.tX + (toff + i) * np + cI) * wi;
+                }
+#pragma unroll
+                for (int cI = 0; cI < kMaxCovariates; ++cI) {
+                    if (cI >= np) break;  // uniform across the CTA
+                    const double v = warp_sum(accq[cI]);
+                    if (lane == 0) red[warp] = v;
+                    __syncthreads();
+                    if (tid == 0) {
+                        double t = 0.0;
+                        for (int w = 0; w < NWARP; ++w) t += red[w];
+                        a.gls_out[s * W + (q == 0 ? np * np + cI : cI * np + (q - 1))] = t;
+                    }
+                    __syncthreads();
+                }
+            }
+            if (tid == 0) a.fail[oi] = 0;
+            fence_proxy_async();
+            __syncthreads();
+            continue;
+        }
+        backsub(k);
 
         // ---------------- prediction and squared error (Eq.3, Eq.4) ----------------
         const double *vx = a.vx + voff, *vy = a.vy + voff, *vv = a.vv + voff;
@@ -597,16 +646,88 @@ __global__ void reduce_kernel(const double *vals, const uint8_t *fail, const int
     if (status) status[c] = (int32_t)st;
 }
 
+// GLS: W = (p+1) p entries per subset; thread w sums entry w over subsets in ascending s
+// (failed subsets poison the sums), then thread 0 solves A beta = b by Gaussian elimination
+// with partial pivoting (largest |pivot|, first on ties).
+__global__ void gls_solve_kernel(const double *part, const uint8_t *fail, int64_t N, int32_t p, double *sums,
+                                 double *beta, int32_t *status) {
+    const int W = (p + 1) * p;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        double acc = 0.0;
+        for (int64_t s = 0; s < N; ++s) acc += fail[s] ? __longlong_as_double(0x7ff8000000000000ll) : part[s * W + w];
+        sums[w] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double A[kMaxCovariates * kMaxCovariates], b[kMaxCovariates];
+    for (int i = 0; i < p * p; ++i) A[i] = sums[i];
+    for (int i = 0; i < p; ++i) b[i] = sums[p * p + i];
+    int32_t st = 0;
+    for (int c = 0; c < p && !st; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < p; ++r)
+            if (fabs(A[r * p + c]) > fabs(A[piv * p + c])) piv = r;
+        if (!(A[piv * p + c] != 0.0)) {
+            st = 1;
+            break;
+        }
+        if (piv != c) {
+            for (int j = 0; j < p; ++j) {
+                const double t = A[c * p + j];
+                A[c * p + j] = A[piv * p + j];
+                A[piv * p + j] = t;
+            }
+            const double t = b[c];
+            b[c] = b[piv];
+            b[piv] = t;
+        }
+        for (int r = c + 1; r < p; ++r) {
+            const double f = A[r * p + c] / A[c * p + c];
+            for (int j = c; j < p; ++j) A[r * p + j] -= f * A[c * p + j];
+            b[r] -= f * b[c];
+        }
+    }
+    for (int r = p - 1; r >= 0; --r) {
+        double sum = b[r];
+        for (int j = r + 1; j < p; ++j) sum -= A[r * p + j] * beta[j];
+        beta[r] = st ? __longlong_as_double(0x7ff8000000000000ll) : sum / A[r * p + r];
+    }
+    *status = st;
+}
+
+__global__ void gather_rows_kernel(int64_t cnt, const int32_t *idx, const double *X, int32_t p, double *out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt * p;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / p;
+        out[e] = X[(int64_t)idx[i] * p + (e - i * p)];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_gls_solve(const double *part, const uint8_t *fail, int64_t N, int32_t p, double *sums,
+                             double *beta, int32_t *status, cudaStream_t st) {
+    gls_solve_kernel<<<1, 128, 0, st>>>(part, fail, N, p, sums, beta, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(int64_t cnt, const int32_t *idx, const double *X, int32_t p, double *out,
+                               cudaStream_t st) {
+    if (cnt == 0) return cudaSuccess;
+    const int64_t total = cnt * p;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    gather_rows_kernel<<<grid, 256, 0, st>>>(cnt, idx, X, p, out);
+    return cudaGetLastError();
+}
 
 size_t cv_kernel_smem_bytes() { return SMEM_BYTES; }
 int cv_kernel_max_k() { return 1 << 20; }  // bounded by the factor workspace, not SMEM
-size_t cv_kernel_slot_doubles(int64_t kmax) {
+size_t cv_kernel_slot_doubles(int64_t kmax, int extra_rows) {
     // column groups x ld x 16 (the factor) + alpha when it does not fit in SMEM + MT x 16:
     // a bulk copy of the last group's row tile may read past row k.  Rounded to 256 B so
     // every slot base keeps the alignment bulk copies need.
     const int64_t groups = (kmax + KC - 1) / KC;
-    const size_t d = (size_t)(groups > 0 ? groups : 1) * (size_t)factor_ld(kmax) * KC +
+    const size_t d = (size_t)(groups > 0 ? groups : 1) * (size_t)factor_ld(kmax + extra_rows) * KC +
                      (size_t)kmax + (size_t)MT * KC;
     return (d + 31) / 32 * 32;
 }

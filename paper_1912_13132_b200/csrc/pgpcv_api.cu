@@ -142,6 +142,7 @@ struct pgpcv_ctx {
     DevBuf<double> bounds;  // ex, lox, hix, ey, loy, hiy
     DevBuf<double> rects, split;      // subset rectangles [N*4]; bisection split per node id
     std::vector<double> h_rects;
+    pgpcv_rect domain{};
     DevBuf<int64_t> train_off2;       // shell-cap output (swapped in)
     DevBuf<int32_t> train_idx2;
     DevBuf<unsigned int> cnt, cur;
@@ -171,6 +172,8 @@ struct pgpcv_ctx {
     DevBuf<double> p_sub, p_yhat, p_sum;
     DevBuf<uint8_t> p_fail;
     DevBuf<int32_t> p_status;
+    // pgpcv_gls
+    DevBuf<double> g_X, g_tX, g_part, g_sums, g_beta;
     // pgpcv_select: the last evaluation's device-resident per-subset losses
     int32_t sel_C = 0;
     DevBuf<double> sel_rmspe, sel_local;
@@ -290,6 +293,7 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     }
     ctx->N = N;
     ctx->n = n;
+    ctx->domain = d;
     // K1 count, K2 scan
     CK(ctx->cnt.ensure(3 * N), "alloc counts");
     CK(ctx->cur.ensure(3 * N), "alloc cursors");
@@ -666,6 +670,9 @@ struct CvLaunch {
     const double *gx = nullptr, *gy = nullptr, *gv = nullptr;
     double *subset_loss = nullptr, *subset_nll = nullptr, *yhat = nullptr;
     uint8_t *fail = nullptr;
+    int32_t p = 0;  // GLS covariates (bordered rows below y)
+    const double *tX = nullptr;
+    double *gls_out = nullptr;
     double flops = 0;
     int slots = 0;
 };
@@ -698,7 +705,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         const int cap = atoi(env);
         if (cap > 0) slots = std::min(slots, cap);
     }
-    const size_t slot_stride = cv_kernel_slot_doubles(kmax);
+    const size_t slot_stride = cv_kernel_slot_doubles(kmax, L.p);
     while (true) {
         cudaError_t e = ctx->work.ensure((size_t)slots * slot_stride);
         if (e == cudaSuccess) break;
@@ -736,6 +743,12 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.subset_nll = L.subset_nll;
         a.yhat = L.yhat;
         a.fail = L.fail;
+        a.p = L.p;
+        a.tX = L.tX;
+        a.rects = ctx->rects.p;
+        a.xmax = ctx->domain.xmax;
+        a.ymax = ctx->domain.ymax;
+        a.gls_out = L.gls_out;
         CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
     }
     CK(cudaEventRecord(ctx->ev[2], st), "event");
@@ -1000,6 +1013,77 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
     record_timing(ctx, L, launches);
     if (sspe) *sspe = total;
     if (status >= 0) return ctx->fail_with(PGPCV_ENUMERIC, "subset %d was not positive definite", status);
+    return PGPCV_OK;
+}
+
+int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, double *beta, double *xtmx,
+              double *xtmy) {
+    if (!ctx) return PGPCV_EINVAL;
+    if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "pgpcv_gls needs a partition");
+    if (p < 1 || p > kMaxCovariates) return ctx->fail_with(PGPCV_EINVAL, "need 1 <= p <= %d covariates", kMaxCovariates);
+    if (!X || !beta) return ctx->fail_with(PGPCV_EINVAL, "NULL X or beta");
+    int rc = check_params(ctx, &param, 1);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t N = ctx->N, n = ctx->n, sum_k = ctx->info.sum_k;
+    const int W = (p + 1) * p;
+    CK(ctx->g_X.ensure((size_t)n * p), "alloc");
+    CK(ctx->g_tX.ensure((size_t)sum_k * p), "alloc");
+    CK(ctx->g_part.ensure((size_t)N * W), "alloc");
+    CK(ctx->g_sums.ensure(W), "alloc");
+    CK(ctx->g_beta.ensure(p), "alloc");
+    CK(ctx->p_fail.ensure(N), "alloc");
+    CK(ctx->p_status.ensure(1), "alloc");
+    CvLaunch L;
+    L.flags = kCvGls;
+    L.params = &param;
+    L.C = 1;
+    L.out_C = 1;
+    L.tgt_off = ctx->val_off.p;
+    L.gx = ctx->vx.p;
+    L.gy = ctx->vy.p;
+    L.gv = ctx->vv.p;
+    L.fail = ctx->p_fail.p;
+    L.p = p;
+    L.tX = ctx->g_tX.p;
+    L.gls_out = ctx->g_part.p;
+    for (int64_t s = 0; s < N; ++s) {
+        const int64_t k = ctx->h_train_off[s + 1] - ctx->h_train_off[s];
+        if (!ctx->owned[s] || k == 0) continue;
+        L.items.push_back(make_int2((int)s, 0));
+        const double kd = (double)k;
+        // Cholesky + (p+1) forward (bordered) and backward solves + core-row sums
+        L.flops += kd * kd * kd / 3.0 + kd * kd / 2.0 + kd / 6.0 + (p + 1) * (2.0 * kd * kd + 2.0 * kd * p);
+    }
+    CK(cudaEventRecord(ctx->ev[0], st), "event");
+    CK(cudaMemcpyAsync(ctx->g_X.p, X, sizeof(double) * n * p, cudaMemcpyHostToDevice, st), "copy X");
+    CK(launch_gather_rows(sum_k, ctx->train_idx.p, ctx->g_X.p, p, ctx->g_tX.p, st), "gather X");
+    CK(cudaMemsetAsync(ctx->g_part.p, 0, sizeof(double) * N * W, st), "memset");
+    CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
+    if ((rc = run_cv(ctx, L))) return rc;
+    int launches = 1 + (L.items.empty() ? 0 : 1);
+    if (ctx->world > 1) {  // exclusive owners: exact sums
+        if ((rc = nccl_sum(ctx, ctx->g_part.p, (size_t)N * W, ncclFloat64))) return rc;
+        if ((rc = nccl_sum(ctx, ctx->p_fail.p, (size_t)N, ncclUint8))) return rc;
+    }
+    CK(launch_gls_solve(ctx->g_part.p, ctx->p_fail.p, N, p, ctx->g_sums.p, ctx->g_beta.p, ctx->p_status.p, st),
+       "gls solve");
+    ++launches;
+    std::vector<double> sums(W);
+    int32_t status = 0;
+    CK(cudaMemcpyAsync(beta, ctx->g_beta.p, sizeof(double) * p, cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaMemcpyAsync(sums.data(), ctx->g_sums.p, sizeof(double) * W, cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaMemcpyAsync(&status, ctx->p_status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaEventRecord(ctx->ev[3], st), "event");
+    CK(cudaStreamSynchronize(st), "gls");
+    CK(cudaGetLastError(), "gls");
+    ctx->cv_done = true;
+    record_timing(ctx, L, launches);
+    if (xtmx) memcpy(xtmx, sums.data(), sizeof(double) * p * p);
+    if (xtmy) memcpy(xtmy, sums.data() + p * p, sizeof(double) * p);
+    if (std::isnan(sums[0])) return ctx->fail_with(PGPCV_ENUMERIC, "a subset was not positive definite");
+    if (status) return ctx->fail_with(PGPCV_ENUMERIC, "X^T M^-1 X is singular");
     return PGPCV_OK;
 }
 

@@ -30,9 +30,17 @@ struct CvArgs {
     double *subset_nll;         // [N*out_C] -2 log-likelihood of the training data (kCvNll)
     double *yhat;               // [sum of targets] kriging predictions, or nullptr
     uint8_t *fail;              // [N*out_C] 1 = not positive definite
+    // kCvGls (row f4): p covariate rows bordered below y; per-subset core-row sums
+    int32_t p;                  // number of covariates (0 unless kCvGls)
+    const double *tX;           // [sum_k * p] staged covariates of the training members
+    const double *rects;        // [N*4] subset rectangles (the cores)
+    double xmax, ymax;          // domain top edges (closed, R3)
+    double *gls_out;            // [N * (p+1) * p]: A (p x p row-major) then b (p)
 };
 constexpr int32_t kCvPredict = 1;  // back-substitution, prediction, SSPE (Eq.3, Eq.4)
 constexpr int32_t kCvNll = 2;      // -2 log-likelihood from the same factor (Eq.2)
+constexpr int32_t kCvGls = 4;      // GLS normal-equation sums from the same factor (Eq. GLS)
+constexpr int32_t kMaxCovariates = 8;
 
 // Kernel geometry (see cv_kernel.cu for the derivation).
 constexpr int kMT = 128;        // rows per row tile
@@ -40,11 +48,17 @@ constexpr int kNB = 64;         // block-column width of the left-looking Choles
 constexpr int kThreads = 256;   // 8 warps
 size_t cv_kernel_smem_bytes();
 int cv_kernel_max_k();
-size_t cv_kernel_slot_doubles(int64_t kmax);  // factor + back-substitution scratch
+size_t cv_kernel_slot_doubles(int64_t kmax, int extra_rows = 0);  // factor + back-substitution scratch
 // leading dimension (doubles) of a k-point factor: column-major (k+1) x k, +1 bordered row
 __host__ __device__ inline int64_t factor_ld(int64_t k) { return ((k + 1 + 15) / 16) * 16; }
 
 cudaError_t launch_cv_kernel(const CvArgs &a, int grid, cudaStream_t st);
+// GLS (row f4): out[w] = sum_s part[s*W + w] in ascending s (W = (p+1) p), then
+// beta = A^{-1} b by Gaussian elimination with partial pivoting; *status = 0 ok, 1 singular.
+cudaError_t launch_gls_solve(const double *part, const uint8_t *fail, int64_t N, int32_t p, double *sums,
+                             double *beta, int32_t *status, cudaStream_t st);
+cudaError_t launch_gather_rows(int64_t cnt, const int32_t *idx, const double *X, int32_t p, double *out,
+                               cudaStream_t st);
 cudaError_t cv_kernel_occupancy(int *blocks_per_sm);
 // out[c] = sum_s vals[s*C + c] over subsets s with mask_off[s+1] > mask_off[s] (all subsets
 // when mask_off is null), in ascending s; NaN (and status[c] = first failing s) on failure.

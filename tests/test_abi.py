@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     lib = pg.load_library()
     for name in _declared_symbols():
         assert hasattr(lib, name), name
-    assert pg.version() == pg.ABI_VERSION == 3
+    assert pg.version() == pg.ABI_VERSION == 4
 
 
 def test_library_is_sm100a_only():
