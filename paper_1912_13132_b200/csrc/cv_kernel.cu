@@ -15,9 +15,10 @@
 // coordinates (distance -> exp), so a config costs no HBM traffic beyond the factor L.
 //
 // Data layout (per resident CTA, in HBM): L has k+1 rows (rows 0..k-1 the Cholesky factor,
-// row k the bordered z) and k columns, stored in column groups of KC = 16: group q holds
-// rows 0..ld-1 (ld = roundup(k+1, 16)) with each row's 16 values contiguous (128 B) and
-// XOR-swizzled by the row,  L(r, c) at ((c>>4)*ld + r)*16 + ((c & 15) ^ 4(r & 3)).
+// row k the bordered z; GLS adds p covariate rows) and k columns, stored in column groups
+// of KC = 16: group q holds rows 16q..ld-1 (ld = roundup(k+1, 16); the packed lower
+// triangle) with each row's 16 values contiguous (128 B) and XOR-swizzled by the row,
+// L(r, c) at (gbase(q) + r)*16 + ((c & 15) ^ 4(r & 3)), q = c >> 4.
 // An operand chunk (MT or NB consecutive rows of one column group) is then one
 // contiguous 16 KB / 8 KB block: one bulk copy, and conflict-free DMMA fragment loads
 // from the unpadded SMEM image.
@@ -126,15 +127,45 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Diagnostic build only (-DPGPCV_PHASE_PROFILE, probes/p2_phases.py): thread 0 of every CTA
+// attributes its clock64() time to the phases below; the API prints the sums per launch.
+#ifdef PGPCV_PHASE_PROFILE
+#define PH_DECL long long ph_t = clock64();
+#define PH(i)                                   \
+    do {                                        \
+        if (tid == 0) {                         \
+            const long long t_ = clock64();     \
+            s_ph[i] += (unsigned long long)(t_ - ph_t); \
+            ph_t = t_;                          \
+        }                                       \
+    } while (0)
+#else
+#define PH_DECL
+#define PH(i) \
+    do {      \
+    } while (0)
+#endif
+// 0 item fetch/setup, 1 block-column setup, 2 A generation, 3 GEMM issue/compute,
+// 4 GEMM operand wait, 5 diagonal block, 6 TRSM + stores, 7 solves/prediction/outputs
+constexpr int kPhases = 8;
+
 constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));  // 24,576 B
 
+// Packed lower-triangular storage: column group q (columns 16q..16q+15) is only ever read or
+// written at rows >= 16q, so it stores rows 16q..ld-1; groups follow each other.  Row r of
+// group q starts at (gbase(q) + r) * 16 with gbase(q) = sum_{q'<q} (ld - 16q') - 16q.
+__host__ __device__ __forceinline__ int64_t gbase(int64_t ld, int64_t q) { return q * ld - 8 * q * (q + 1); }
+// doubles of a packed factor with G column groups
+__host__ __device__ __forceinline__ int64_t factor_doubles(int64_t ld, int64_t G) {
+    return (G * ld - 8 * G * (G - 1)) * KC;
+}
 // Element (r, c) of the factor in the column-group tiled, row-swizzled layout.
 __device__ __forceinline__ size_t lidx(int64_t ld, int r, int c) {
-    return ((size_t)(c >> 4) * ld + r) * KC + ((c & 15) ^ ((r & 3) << 2));
+    return (size_t)(gbase(ld, c >> 4) + r) * KC + ((c & 15) ^ ((r & 3) << 2));
 }
 // Start of the contiguous chunk rows r.. of column group q.
 __device__ __forceinline__ const double *lchunk(const double *L, int64_t ld, int q, int r) {
-    return L + ((size_t)q * ld + r) * KC;
+    return L + (size_t)(gbase(ld, q) + r) * KC;
 }
 
 // Operand chunk n of the running sequence (stage n % STAGES, use n / STAGES): one thread
@@ -183,6 +214,10 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     __shared__ __align__(8) uint64_t empty[STAGES];
     __shared__ int s_item;
     __shared__ int s_fail;
+#ifdef PGPCV_PHASE_PROFILE
+    __shared__ unsigned long long s_ph[kPhases];
+    if (threadIdx.x < kPhases) s_ph[threadIdx.x] = 0;
+#endif
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -198,13 +233,20 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     }
     __syncthreads();
     uint32_t pc = 0;  // operand chunks consumed so far (identical in every thread)
+    PH_DECL
 
     for (;;) {
         if (tid == 0) s_item = (int)atomicAdd(a.counter, 1u);
         __syncthreads();
         const int item = s_item;
         __syncthreads();
-        if (item >= a.n_items) break;
+        if (item >= a.n_items) {
+#ifdef PGPCV_PHASE_PROFILE
+            PH(0);
+            if (tid < kPhases && a.prof) a.prof[blockIdx.x * kPhases + tid] = s_ph[tid];
+#endif
+            break;
+        }
         const int s = a.items[item].x;
         const int c = a.items[item].y;
         const int64_t toff = a.train_off[s];
@@ -241,9 +283,11 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             // The previous block column's factor stores (generic proxy, made GPU-visible
             // before the last barrier) are read next by bulk copies (async proxy); the
             // stage memory was last touched by generic accesses (LJ, alpha).
+            PH(0);
             if (tid == 0) tile_prologue(pc, nk, stage, full, empty, L, ld, j0, j0);
             __syncwarp();
             __syncthreads();  // cx/cy/cv visible
+            PH(1);
             for (int rt = 0; rt < ntiles; ++rt) {
                 const int r0 = j0 + rt * MT;
                 const int rbase = r0 + warp * 16;  // this warp's first row
@@ -282,6 +326,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                             }
                 }
 
+                PH(2);
                 // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
                 for (int kc = 0; kc < nk; ++kc) {
@@ -293,7 +338,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         if (kc + STAGES - 1 + PFD < nk)
                             prefetch_chunk(L, ld, r0, j0, (kc + STAGES - 1 + PFD) * KC);
                     }
+                    PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
+                    PH(4);
                     __syncwarp();  // mma.sync.aligned needs the whole warp converged
                     const double *As = stage + (n % STAGES) * (A_STAGE + B_STAGE);
                     const double *ap = As + (warp * 16 + g) * KC + t;
@@ -320,6 +367,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     if (lane == 0) mbar_arrive(&empty[n % STAGES]);
                 }
                 pc += nk;
+                PH(3);
                 // Columns past the matrix (last block column) came from rows of the
                 // workspace beyond the factor: force C = 0 there (Linv^T is 0 there too).
 #pragma unroll
@@ -389,6 +437,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     __syncthreads();      // LJ (stage memory) dead from here on
                 }
 
+                PH(5);
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
                 if (rt + 1 < ntiles && tid == 0) tile_prologue(pc, nk, stage, full, empty, L, ld, r0 + MT, j0);
@@ -452,6 +501,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     fence_proxy_async();
                     __syncthreads();
                 }
+                PH(6);
             }
         }
 
@@ -501,7 +551,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         // alpha (k doubles) and the per-warp partial sums (NWARP x NB) live in the stage
         // buffers when they fit, else alpha goes to the slot's scratch after the factor.
         const bool alpha_smem = k + NWARP * NB <= STAGE_DBL;
-        double *alpha = alpha_smem ? stage : L + (size_t)((k + KC - 1) / KC) * ld * KC;
+        double *alpha = alpha_smem ? stage : L + factor_doubles(ld, (k + KC - 1) / KC);
         double *part2 = alpha_smem ? stage + STAGE_DBL - NWARP * NB : stage;
         double *LB = Bt;        // diagonal block, [row][col] stride LJS
         double *tvec = cx;      // NB
@@ -521,7 +571,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 if (c0 < jw) {
                     for (int r = rs + warp; r < k; r += NWARP) {
                         const double ar = alpha[r];
-                        const double *row = L + ((size_t)grp * ld + r) * KC;
+                        const double *row = L + (size_t)(gbase(ld, grp) + r) * KC;
                         const int sw = (r & 3) << 2;
                         p0 += __ldcg(row + ((c0 & 15) ^ sw)) * ar;
                         p1 += __ldcg(row + (((c0 + 1) & 15) ^ sw)) * ar;
@@ -621,6 +671,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             a.subset_loss[oi] = l;
             a.fail[oi] = 0;
         }
+        PH(7);
     }
 }
 
@@ -723,11 +774,11 @@ cudaError_t launch_gather_rows(int64_t cnt, const int32_t *idx, const double *X,
 size_t cv_kernel_smem_bytes() { return SMEM_BYTES; }
 int cv_kernel_max_k() { return 1 << 20; }  // bounded by the factor workspace, not SMEM
 size_t cv_kernel_slot_doubles(int64_t kmax, int extra_rows) {
-    // column groups x ld x 16 (the factor) + alpha when it does not fit in SMEM + MT x 16:
-    // a bulk copy of the last group's row tile may read past row k.  Rounded to 256 B so
+    // the packed factor + alpha when it does not fit in SMEM + MT x 16: a bulk copy of the
+    // last group's row tile may read past the factor's end.  Rounded to 256 B so
     // every slot base keeps the alignment bulk copies need.
     const int64_t groups = (kmax + KC - 1) / KC;
-    const size_t d = (size_t)(groups > 0 ? groups : 1) * (size_t)factor_ld(kmax + extra_rows) * KC +
+    const size_t d = (size_t)factor_doubles(factor_ld(kmax + extra_rows), groups > 0 ? groups : 1) +
                      (size_t)kmax + (size_t)MT * KC;
     return (d + 31) / 32 * 32;
 }

@@ -174,6 +174,7 @@ struct pgpcv_ctx {
     DevBuf<int32_t> p_status;
     // pgpcv_gls
     DevBuf<double> g_X, g_tX, g_part, g_sums, g_beta;
+    DevBuf<unsigned long long> prof;  // diagnostic phase cycles (-DPGPCV_PHASE_PROFILE)
     // pgpcv_select: the last evaluation's device-resident per-subset losses
     int32_t sel_C = 0;
     DevBuf<double> sel_rmspe, sel_local;
@@ -749,7 +750,26 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.xmax = ctx->domain.xmax;
         a.ymax = ctx->domain.ymax;
         a.gls_out = L.gls_out;
+        a.prof = nullptr;
+#ifdef PGPCV_PHASE_PROFILE
+        CK(ctx->prof.ensure((size_t)slots * 8), "alloc prof");
+        CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 8, st), "memset");
+        a.prof = ctx->prof.p;
+#endif
         CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
+#ifdef PGPCV_PHASE_PROFILE
+        {
+            std::vector<unsigned long long> h((size_t)slots * 8);
+            CK(cudaMemcpyAsync(h.data(), ctx->prof.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
+                               st), "copy prof");
+            CK(cudaStreamSynchronize(st), "prof");
+            double sum[8] = {0};
+            for (int b = 0; b < slots; ++b)
+                for (int i = 0; i < 8; ++i) sum[i] += (double)h[(size_t)b * 8 + i];
+            fprintf(stderr, "PGPCV_PHASES {\"slots\": %d, \"cycles\": [%.6e, %.6e, %.6e, %.6e, %.6e, %.6e, %.6e, %.6e]}\n",
+                    slots, sum[0], sum[1], sum[2], sum[3], sum[4], sum[5], sum[6], sum[7]);
+        }
+#endif
     }
     CK(cudaEventRecord(ctx->ev[2], st), "event");
     return PGPCV_OK;

@@ -1,0 +1,45 @@
+"""P2 -- where the cv_kernel's time goes: runs one c5 (or c6) configuration through the
+diagnostic build libpgpcv_phases.so (-DPGPCV_PHASE_PROFILE: thread 0 of every CTA
+attributes its clock64() time to 8 phases) and prints the phase shares as JSON."""
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NAMES = ["item_setup", "column_setup", "A_generation", "gemm_issue", "gemm_operand_wait",
+         "diagonal_block", "trsm_store", "solve_predict"]
+
+if len(sys.argv) > 1 and sys.argv[1] == "child":
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import torch
+    import paper_1912_13132_b200 as pg
+    import workloads
+    wname = sys.argv[2]
+    w = workloads.make(wname, device="cuda")
+    with pg.Context(0) as ctx:
+        if w.depth is None:
+            ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+        else:
+            ctx.partition_bisect(w.x, w.y, w.value, w.role, w.domain, w.depth, w.delta, w.shell_cap, w.cap_seed)
+        ctx.cv_loss(np.array([[1.0, 1.0, 0.1]]), want_subset_loss=False)
+        t = ctx.last_timing()
+        print("TIMING", json.dumps(t), flush=True)
+    sys.exit(0)
+
+wname = sys.argv[1] if len(sys.argv) > 1 else "c5"
+env = dict(os.environ, PGPCV_LIB=os.path.join(ROOT, "paper_1912_13132_b200", "libpgpcv_phases.so"))
+r = subprocess.run([sys.executable, __file__, "child", wname], env=env, capture_output=True, text=True)
+m = re.search(r"PGPCV_PHASES (\{.*\})", r.stderr)
+t = re.search(r"TIMING (\{.*\})", r.stdout)
+if not m:
+    sys.stderr.write(r.stdout + r.stderr)
+    sys.exit(1)
+d = json.loads(m.group(1))
+cyc = d["cycles"]
+tot = sum(cyc)
+out = {"workload": wname, "slots": d["slots"], "timing": json.loads(t.group(1)) if t else None,
+       "share": {n: round(c / tot, 4) for n, c in zip(NAMES, cyc)}}
+print(json.dumps(out))
