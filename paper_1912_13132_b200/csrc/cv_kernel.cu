@@ -68,7 +68,7 @@ constexpr int B_STAGE = NB * KC;                         // 1,024 doubles (8 KB)
 constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE);  // 9,216 doubles
 constexpr int BT_DBL = NB * BS;                          // Linv^T tile
 constexpr int COL_DBL = 3 * NB;                          // block-column x, y, value
-constexpr int MISC_DBL = NB + NWARP;                     // sqrt pivots, warp partials
+constexpr int MISC_DBL = NB + NWARP + 64;                // sqrt pivots, warp partials, exp table
 constexpr size_t SMEM_BYTES = sizeof(double) * (STAGE_DBL + BT_DBL + COL_DBL + MISC_DBL);
 static_assert(NB * LJS <= STAGE_DBL, "diagonal block must fit in the stage buffers");
 static_assert(NB * LJS <= BT_DBL, "back-substitution block must fit in the Linv buffer");
@@ -146,8 +146,54 @@ __device__ __forceinline__ double warp_sum(double v) {
     } while (0)
 #endif
 // 0 item fetch/setup, 1 block-column setup, 2 A generation, 3 GEMM issue/compute,
-// 4 GEMM operand wait, 5 diagonal block, 6 TRSM + stores, 7 solves/prediction/outputs
-constexpr int kPhases = 8;
+// 4 GEMM operand wait, 5 barrier after tile 0's GEMM, 6 diagonal factorization + inverse,
+// 7 L_jj store + barrier, 8 TRSM + stores, 9 end-of-column fence + barrier,
+// 10 back-substitution, 11 prediction + outputs
+constexpr int kPhases = 12;
+
+// exp(x) for x <= 0 (x = -d/theta, the exponential covariance), table-driven:
+// x = (64 n + j) ln2/64 + r with |r| <= ln2/128, exp(x) = 2^n * T[j] * (1 + p(r)), T[j] =
+// 2^(j/64) from SMEM, p the degree-5 Taylor polynomial (truncation r^6/720 < 0.3 ulp).
+// Max error < 1 ulp over [-708, 0] (checked against a 60-digit reference); 10 FP64 ops
+// instead of the ~20 of the general exp().  The FP64 pipe is shared with the co-resident
+// CTA's DMMA stream, so shortening these serial chains shortens the epilogue.
+constexpr int EXP_TAB = 64;
+// 2^(j/64), j = 0..63, correctly rounded (computed to 60 digits; copied to SMEM per CTA)
+__constant__ double kExp2Tab[EXP_TAB] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951,
+};
+__device__ __forceinline__ double exp_neg(double x, const double *tab) {
+    const double kShift = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
+    const double t = fma(x, 92.33248261689366, kShift);  // x * 64/ln2 + shift
+    const int ki = __double2loint(t);
+    const double kf = t - kShift;
+    double r = fma(kf, -0.010830424696223417, x);  // ln2/64, high 36 bits
+    r = fma(kf, -2.572804622327669e-14, r);        // ln2/64, low part
+    double p = fma(8.333333333333333e-03, r, 4.1666666666666664e-02);
+    p = fma(p, r, 0.16666666666666666);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p *= r;
+    const double tj = tab[ki & (EXP_TAB - 1)];
+    const double m = fma(tj, p, tj);
+    const double res = __hiloint2double(__double2hiint(m) + ((ki >> 6) << 20), __double2loint(m));
+    return x < -708.0 ? 0.0 : res;
+}
 
 constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));  // 24,576 B
 
@@ -210,6 +256,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     double *cv = cy + NB;
     double *dg = cv + NB;               // sqrt pivots of the diagonal block
     double *red = dg + NB;              // per-warp partial sums
+    double *etab = red + NWARP;         // 2^(j/64), j = 0..63 (exp_neg)
     __shared__ __align__(8) uint64_t full[STAGES];
     __shared__ __align__(8) uint64_t empty[STAGES];
     __shared__ int s_item;
@@ -224,6 +271,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     const int g = lane >> 2, t = lane & 3;
     double *L = a.work + (size_t)blockIdx.x * a.slot_stride;
 
+    if (tid < EXP_TAB) etab[tid] = kExp2Tab[tid];
     if (tid == 0) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
@@ -303,6 +351,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         rx[i] = r < k ? __ldg(tx + r) : 0.0;
                         ry[i] = r < k ? __ldg(ty + r) : 0.0;
                     }
+                    // all 32 entries without branches (independent chains the scheduler can
+                    // interleave); the special entries by selects
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -312,18 +362,26 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 const int r = rbase + i * 8 + g;
                                 const int nl = j * 8 + 2 * t + e;
                                 const int cc = j0 + nl;
-                                double av;
-                                if (cc >= k || r > kb) av = 0.0;
-                                else if (r == k) av = cv[nl];        // bordered row: y_T
-                                else if (r > k) av = __ldg(a.tX + (toff + cc) * np + (r - k - 1));
-                                else if (r == cc) av = 1.0 + lam;    // exp(0) + lambda
-                                else if (r < cc) av = 0.0;           // upper triangle: unused
-                                else {
-                                    const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
-                                    av = exp(sqrt(dx * dx + dy * dy) * ninv);
-                                }
-                                acc[i][j][e] = -av;
+                                const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
+                                double v = -exp_neg(sqrt(dx * dx + dy * dy) * ninv, etab);
+                                v = r == cc ? -(1.0 + lam) : v;                 // exp(0) + lambda
+                                v = r == k ? -cv[nl] : v;                       // bordered y_T
+                                v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
+                                acc[i][j][e] = v;
                             }
+                    if (np > 0) {  // bordered covariate rows (GLS, row f4)
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int r = rbase + i * 8 + g;
+                                    const int cc = j0 + j * 8 + 2 * t + e;
+                                    if (r > k && r <= kb && cc < k)
+                                        acc[i][j][e] = -__ldg(a.tX + (toff + cc) * np + (r - k - 1));
+                                }
+                    }
                 }
 
                 PH(2);
@@ -378,6 +436,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 
                 if (rt == 0) {
                     __syncthreads();  // every warp is past the update: LJ may reuse the stages
+                    PH(5);
                     // Diagonal block C = -acc to SMEM, then fused unblocked Cholesky + inverse.
                     if (warp < NB / 16) {
 #pragma unroll
@@ -403,8 +462,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                             if (tid == 0) s_fail = 1;
                             break;
                         }
-                        const double sd = sqrt(d);
-                        const double inv = 1.0 / sd;
+                        const double inv = rsqrt(d);  // one serial chain: 1/sqrt(d), sqrt(d) = d/sqrt(d)
+                        const double sd = d * inv;
                         if (tid == 0) dg[q] = sd;
                         if (cg == 0 && r > q && r < jw) LJ[r * LJS + q] *= inv;
                         if (cg == 1 && r <= q) Bt[r * BS + q] *= inv;
@@ -427,6 +486,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         for (int q = lane; q < jw; q += 32) l += log(dg[q]);
                         logdet += warp_sum(l);
                     }
+                    PH(6);
                     // L_jj -> the factor (lower triangle; the diagonal from the pivots)
                     for (int e = tid; e < jw * jw; e += NT) {
                         const int rr = e / jw, cc = e % jw;
@@ -435,9 +495,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     }
                     fence_proxy_async();  // generic LJ accesses before bulk copies refill it
                     __syncthreads();      // LJ (stage memory) dead from here on
+                    PH(7);
                 }
 
-                PH(5);
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
                 if (rt + 1 < ntiles && tid == 0) tile_prologue(pc, nk, stage, full, empty, L, ld, r0 + MT, j0);
@@ -492,6 +552,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                     L[lidx(ld, r, j0 + nl)] = -xo[i][j][e];
                             }
                 }
+                PH(8);
                 if (rt == ntiles - 1) {
                     // The factor columns just written (generic proxy) are re-read by bulk
                     // copies (async proxy) and ld.global.cg in later block columns and the
@@ -501,7 +562,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     fence_proxy_async();
                     __syncthreads();
                 }
-                PH(6);
+                PH(9);
             }
         }
 
@@ -589,6 +650,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 double sum = 0.0;
                 for (int w = 0; w < NWARP; ++w) sum += part2[w * NB + tid];
                 tvec[tid] = __ldcg(L + lidx(ld, rrow, j0 + tid)) - sum;  // z_c - L[c+1:, c] . alpha
+                dg[tid] = 1.0 / LB[tid * LJS + tid];  // reciprocals off the serial sweep below
             }
             __syncthreads();
             if (warp == 0) {
@@ -596,7 +658,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 double t1 = lane + 32 < jw ? tvec[lane + 32] : 0.0;
                 for (int cc = jw - 1; cc >= 0; --cc) {
                     const double tc = __shfl_sync(0xffffffffu, cc < 32 ? t0 : t1, cc & 31);
-                    const double al = tc / LB[cc * LJS + cc];
+                    const double al = tc * dg[cc];
                     if (lane < cc) t0 -= LB[cc * LJS + lane] * al;
                     if (lane + 32 < cc) t1 -= LB[cc * LJS + lane + 32] * al;
                     if (lane == 0) alpha[j0 + cc] = al;
@@ -646,6 +708,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             continue;
         }
         backsub(k);
+        PH(10);
 
         // ---------------- prediction and squared error (Eq.3, Eq.4) ----------------
         const double *vx = a.vx + voff, *vy = a.vy + voff, *vv = a.vv + voff;
@@ -655,7 +718,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             double sum = 0.0;
             for (int j = lane; j < k; j += 32) {
                 const double dx = px - __ldg(tx + j), dy = py - __ldg(ty + j);
-                sum += exp(sqrt(dx * dx + dy * dy) * ninv) * alpha[j];
+                sum += exp_neg(sqrt(dx * dx + dy * dy) * ninv, etab) * alpha[j];
             }
             sum = warp_sum(sum);
             if (a.yhat && lane == 0) a.yhat[voff + v] = sum;
@@ -671,7 +734,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             a.subset_loss[oi] = l;
             a.fail[oi] = 0;
         }
-        PH(7);
+        PH(11);
     }
 }
 

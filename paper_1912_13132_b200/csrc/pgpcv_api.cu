@@ -752,22 +752,23 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.gls_out = L.gls_out;
         a.prof = nullptr;
 #ifdef PGPCV_PHASE_PROFILE
-        CK(ctx->prof.ensure((size_t)slots * 8), "alloc prof");
-        CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 8, st), "memset");
+        CK(ctx->prof.ensure((size_t)slots * 12), "alloc prof");
+        CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 12, st), "memset");
         a.prof = ctx->prof.p;
 #endif
         CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
 #ifdef PGPCV_PHASE_PROFILE
         {
-            std::vector<unsigned long long> h((size_t)slots * 8);
+            std::vector<unsigned long long> h((size_t)slots * 12);
             CK(cudaMemcpyAsync(h.data(), ctx->prof.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
                                st), "copy prof");
             CK(cudaStreamSynchronize(st), "prof");
-            double sum[8] = {0};
+            double sum[12] = {0};
             for (int b = 0; b < slots; ++b)
-                for (int i = 0; i < 8; ++i) sum[i] += (double)h[(size_t)b * 8 + i];
-            fprintf(stderr, "PGPCV_PHASES {\"slots\": %d, \"cycles\": [%.6e, %.6e, %.6e, %.6e, %.6e, %.6e, %.6e, %.6e]}\n",
-                    slots, sum[0], sum[1], sum[2], sum[3], sum[4], sum[5], sum[6], sum[7]);
+                for (int i = 0; i < 12; ++i) sum[i] += (double)h[(size_t)b * 12 + i];
+            fprintf(stderr, "PGPCV_PHASES {\"slots\": %d, \"cycles\": [", slots);
+            for (int i = 0; i < 12; ++i) fprintf(stderr, "%s%.6e", i ? ", " : "", sum[i]);
+            fprintf(stderr, "]}\n");
         }
 #endif
     }

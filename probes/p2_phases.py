@@ -9,7 +9,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = ["item_setup", "column_setup", "A_generation", "gemm_issue", "gemm_operand_wait",
-         "diagonal_block", "trsm_store", "solve_predict"]
+         "tile0_barrier", "diag_factor", "diag_store", "trsm_store", "column_end_fence",
+         "back_substitution", "predict_outputs"]
 
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.path.insert(0, ROOT)
