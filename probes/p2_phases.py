@@ -31,7 +31,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.exit(0)
 
 wname = sys.argv[1] if len(sys.argv) > 1 else "c5"
-env = dict(os.environ, PGPCV_LIB=os.path.join(ROOT, "paper_1912_13132_b200", "libpgpcv_phases.so"))
+lib = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "paper_1912_13132_b200", "libpgpcv_phases.so")
+env = dict(os.environ, PGPCV_LIB=lib)
 r = subprocess.run([sys.executable, __file__, "child", wname], env=env, capture_output=True, text=True)
 m = re.search(r"PGPCV_PHASES (\{.*\})", r.stderr)
 t = re.search(r"TIMING (\{.*\})", r.stdout)
@@ -41,6 +42,6 @@ if not m:
 d = json.loads(m.group(1))
 cyc = d["cycles"]
 tot = sum(cyc)
-out = {"workload": wname, "slots": d["slots"], "timing": json.loads(t.group(1)) if t else None,
+out = {"workload": wname, "lib": os.path.basename(lib), "slots": d["slots"], "timing": json.loads(t.group(1)) if t else None,
        "share": {n: round(c / tot, 4) for n, c in zip(NAMES, cyc)}}
 print(json.dumps(out))
