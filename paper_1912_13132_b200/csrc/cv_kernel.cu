@@ -68,9 +68,9 @@ constexpr int B_STAGE = NB * KC;                         // 1,024 doubles (8 KB)
 constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE);  // 9,216 doubles
 constexpr int BT_DBL = NB * BS;                          // Linv^T tile
 constexpr int COL_DBL = 3 * NB;                          // block-column x, y, value
-constexpr int MISC_DBL = NB + NWARP + 64;                // sqrt pivots, warp partials, exp table
+constexpr int MISC_DBL = 2 * NB + NWARP + 64;            // pivots, reciprocals, warp partials, exp table
 constexpr size_t SMEM_BYTES = sizeof(double) * (STAGE_DBL + BT_DBL + COL_DBL + MISC_DBL);
-static_assert(NB * LJS <= STAGE_DBL, "diagonal block must fit in the stage buffers");
+static_assert(2 * NB * LJS <= STAGE_DBL, "diagonal block and its inverse must fit in the stage buffers");
 static_assert(NB * LJS <= BT_DBL, "back-substitution block must fit in the Linv buffer");
 static_assert(SMEM_BYTES <= 115712, "two CTAs per SM");
 static_assert((BS * 2) % 32 == 8, "fragment-load stride of Linv^T");
@@ -119,6 +119,24 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
         : "+d"(d[0]), "+d"(d[1])
         : "d"(a), "d"(b));
+}
+
+// One operand chunk (KC = 16 columns) of the update for the warp's NI 8-row fragments.
+template <int NI>
+__device__ __forceinline__ void mma_chunk(double (&acc)[2][8][2], const double *ap, const double *bp, int sw) {
+#pragma unroll
+    for (int k4 = 0; k4 < 16 / 4; ++k4) {
+        const int o = (k4 << 2) ^ sw;
+        double af[2], bf[8];
+        af[0] = ap[o];
+        af[1] = NI > 1 ? ap[8 * 16 + o] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * 16 + o];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int i = 0; i < NI; ++i) dmma(acc[i][j], af[i], bf[j]);
+    }
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -255,12 +273,14 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     double *cy = cx + NB;
     double *cv = cy + NB;
     double *dg = cv + NB;               // sqrt pivots of the diagonal block
-    double *red = dg + NB;              // per-warp partial sums
+    double *rdg = dg + NB;              // reciprocal pivots
+    double *red = rdg + NB;             // per-warp partial sums
     double *etab = red + NWARP;         // 2^(j/64), j = 0..63 (exp_neg)
     __shared__ __align__(8) uint64_t full[STAGES];
     __shared__ __align__(8) uint64_t empty[STAGES];
     __shared__ int s_item;
     __shared__ int s_fail;
+    __shared__ int s_rank;  // arrival order of this CTA on its SM (sched 1)
 #ifdef PGPCV_PHASE_PROFILE
     __shared__ unsigned long long s_ph[kPhases];
     if (threadIdx.x < kPhases) s_ph[threadIdx.x] = 0;
@@ -278,13 +298,25 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             mbar_init(&empty[i], NWARP);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        s_rank = a.sched == 1 ? (int)(atomicAdd(a.counter + 1 + (smid % kMaxSms), 1ull) & 1ull) : 0;
     }
     __syncthreads();
     uint32_t pc = 0;  // operand chunks consumed so far (identical in every thread)
     PH_DECL
 
     for (;;) {
-        if (tid == 0) s_item = (int)atomicAdd(a.counter, 1u);
+        if (tid == 0) {
+            // Claim the next item: from the front of the LPT list, or (sched 1, the SM's
+            // second CTA) from the back, so the two CTAs sharing an SM work on subsets of
+            // different sizes and their non-GEMM phases do not fall into step.  The sum of
+            // both claim counts orders the claims: exactly n_items succeed, none twice.
+            const bool back = a.sched == 1 && s_rank == 1;
+            const unsigned long long old = atomicAdd(a.counter, back ? (1ull << 32) : 1ull);
+            const long long f = (long long)(old & 0xffffffffull), b = (long long)(old >> 32);
+            s_item = f + b < a.n_items ? (int)(back ? a.n_items - 1 - b : f) : a.n_items;
+        }
         __syncthreads();
         const int item = s_item;
         __syncthreads();
@@ -387,6 +419,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 PH(2);
                 // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
+                const int nact = rbase > kb ? 0 : (rbase + 8 > kb ? 1 : 2);  // live 8-row fragments
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
                     if (tid == 0) {
@@ -403,19 +436,10 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     const double *As = stage + (n % STAGES) * (A_STAGE + B_STAGE);
                     const double *ap = As + (warp * 16 + g) * KC + t;
                     const double *bp = As + A_STAGE + g * KC + t;
-#pragma unroll
-                    for (int k4 = 0; k4 < KC / 4; ++k4) {
-                        const int o = (k4 << 2) ^ sw;
-                        double af[2], bf[8];
-                        af[0] = ap[o];
-                        af[1] = ap[8 * KC + o];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * KC + o];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-#pragma unroll
-                            for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
-                    }
+                    // Fragments wholly below the last bordered row (the padding of a tile
+                    // that overhangs the matrix) issue no DMMA: warp-uniform branch.
+                    if (nact == 2) mma_chunk<2>(acc, ap, bp, sw);
+                    else if (nact == 1) mma_chunk<1>(acc, ap, bp, sw);
                     // Release the stage: this warp's generic-proxy reads of it must be
                     // ordered before the async-proxy bulk copy that will refill it (the
                     // mbarrier alone orders only within the generic proxy; without this
@@ -450,29 +474,94 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                     if (nl <= rl) LJ[rl * LJS + nl] = -acc[i][j][e];
                                 }
                     }
-                    for (int e = tid; e < BT_DBL; e += NT) Bt[e] = 0.0;
+                    // Blocked Cholesky of C[0:jw, 0:jw] in panels of 8 columns with the inverse
+                    // built alongside (R = I - sum L Linv, rows finished panel by panel):
+                    //   warp 0: factor the panel (rsqrt pivots, register shuffles, no CTA
+                    //           barrier) and finish the panel's rows of Linv;
+                    //   all:    trailing update of C and R by the panel (8 FMAs per entry).
+                    // 16 CTA barriers per diagonal block instead of 128.
+                    double *RI = LJ + NB * LJS;  // R / Linv rows, [n][q] stride LJS
+                    for (int e = tid; e < NB * LJS; e += NT) RI[e] = (e / LJS == e % LJS) ? 1.0 : 0.0;
                     if (tid == 0) s_fail = 0;
                     __syncthreads();
-                    if (tid < NB) Bt[tid * BS + tid] = 1.0;
-                    __syncthreads();
-                    const int r = tid & (NB - 1), cg = tid >> 6;  // row, column group (0..3)
-                    for (int q = 0; q < jw; ++q) {
-                        const double d = LJ[q * LJS + q];
-                        if (!(d > 0.0)) {  // not positive definite (R12); uniform decision
-                            if (tid == 0) s_fail = 1;
-                            break;
+                    for (int p0 = 0; p0 < jw; p0 += 8) {
+                        const int pw = min(8, jw - p0);
+                        if (warp == 0) {
+                            const int ra = p0 + lane, rb = p0 + 32 + lane;
+                            double va[8], vb[8];
+#pragma unroll
+                            for (int c2 = 0; c2 < 8; ++c2) {
+                                va[c2] = (ra < jw && c2 < pw) ? LJ[ra * LJS + p0 + c2] : 0.0;
+                                vb[c2] = (rb < jw && c2 < pw) ? LJ[rb * LJS + p0 + c2] : 0.0;
+                            }
+                            bool bad = false;
+#pragma unroll
+                            for (int c2 = 0; c2 < 8; ++c2) {
+                                if (c2 < pw && !bad) {
+                                    const double piv = __shfl_sync(0xffffffffu, va[c2], c2);
+                                    if (!(piv > 0.0)) {  // not positive definite (R12); warp-uniform
+                                        bad = true;
+                                    } else {
+                                        const double inv = rsqrt(piv);
+                                        const double sd = piv * inv;
+                                        if (lane == 0) {
+                                            dg[p0 + c2] = sd;
+                                            rdg[p0 + c2] = inv;
+                                        }
+                                        va[c2] = lane == c2 ? sd : (lane > c2 ? va[c2] * inv : va[c2]);
+                                        vb[c2] *= inv;
+#pragma unroll
+                                        for (int c3 = c2 + 1; c3 < 8; ++c3) {
+                                            const double l = __shfl_sync(0xffffffffu, va[c2], c3);
+                                            va[c3] -= va[c2] * l;
+                                            vb[c3] -= vb[c2] * l;
+                                        }
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int c2 = 0; c2 < 8; ++c2) {
+                                if (c2 < pw && ra < jw && lane >= c2) LJ[ra * LJS + p0 + c2] = va[c2];
+                                if (c2 < pw && rb < jw) LJ[rb * LJS + p0 + c2] = vb[c2];
+                            }
+                            if (bad && lane == 0) s_fail = 1;
+                            __syncwarp();
+                            // the panel's rows of Linv: Linv[r] = (R[r] - sum_{i2<i} L[r][p0+i2] Linv[p0+i2]) / L[r][r]
+                            if (!bad) {
+                                for (int i = 0; i < pw; ++i) {
+                                    const int r = p0 + i;
+#pragma unroll
+                                    for (int h = 0; h < 2; ++h) {
+                                        const int q = lane + 32 * h;
+                                        if (q <= r) {
+                                            double v = RI[r * LJS + q];
+                                            for (int i2 = 0; i2 < i; ++i2)
+                                                v -= LJ[r * LJS + p0 + i2] * RI[(p0 + i2) * LJS + q];
+                                            RI[r * LJS + q] = v * rdg[r];
+                                        }
+                                    }
+                                    __syncwarp();
+                                }
+                            }
                         }
-                        const double inv = rsqrt(d);  // one serial chain: 1/sqrt(d), sqrt(d) = d/sqrt(d)
-                        const double sd = d * inv;
-                        if (tid == 0) dg[q] = sd;
-                        if (cg == 0 && r > q && r < jw) LJ[r * LJS + q] *= inv;
-                        if (cg == 1 && r <= q) Bt[r * BS + q] *= inv;
                         __syncthreads();
-                        if (r > q && r < jw) {
-                            const double lrq = LJ[r * LJS + q];
-                            for (int cc = q + 1 + cg; cc <= r; cc += 4)
-                                LJ[r * LJS + cc] -= lrq * LJ[cc * LJS + q];
-                            for (int i = cg; i <= q; i += 4) Bt[i * BS + r] -= lrq * Bt[i * BS + q];
+                        if (s_fail) break;  // uniform
+                        const int p1 = p0 + pw;
+                        if (p1 < jw) {
+                            const int mt = jw - p1;
+                            for (int e = tid; e < mt * mt; e += NT) {  // C[rr][cc] -= L[rr][panel] . L[cc][panel]
+                                const int rr = p1 + e / mt, cc = p1 + e % mt;
+                                if (cc > rr) continue;
+                                double v = LJ[rr * LJS + cc];
+                                for (int i = 0; i < pw; ++i) v -= LJ[rr * LJS + p0 + i] * LJ[cc * LJS + p0 + i];
+                                LJ[rr * LJS + cc] = v;
+                            }
+                            for (int e = tid; e < mt * p1; e += NT) {  // R[rr][q] -= L[rr][panel] . Linv[panel][q]
+                                const int rr = p1 + e / p1, q = e % p1;
+                                double v = RI[rr * LJS + q];
+                                for (int i = 0; i < pw; ++i) v -= LJ[rr * LJS + p0 + i] * RI[(p0 + i) * LJS + q];
+                                RI[rr * LJS + q] = v;
+                            }
                         }
                         __syncthreads();
                     }
@@ -481,6 +570,12 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         failed = true;
                         break;
                     }
+                    // Linv^T for the TRSM-as-GEMM: Bt[q][n] = Linv[n][q] (zero outside the block)
+                    for (int e = tid; e < NB * NB; e += NT) {
+                        const int q = e / NB, nn = e % NB;
+                        Bt[q * BS + nn] = (q <= nn && nn < jw) ? RI[nn * LJS + q] : 0.0;
+                    }
+                    __syncthreads();
                     if ((a.flags & kCvNll) && warp == 0) {  // log det of this diagonal block
                         double l = 0.0;
                         for (int q = lane; q < jw; q += 32) l += log(dg[q]);
@@ -538,7 +633,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         for (int j = 0; j < 4; ++j)
 #pragma unroll
                             for (int i = 0; i < 2; ++i)
-                                if (sl <= 2 * (h * 4 + j) + 1) dmma(xo[i][j], af[i], bf[j]);
+                                if (sl <= 2 * (h * 4 + j) + 1 && i < nact) dmma(xo[i][j], af[i], bf[j]);
                     }
 #pragma unroll
                     for (int i = 0; i < 2; ++i)

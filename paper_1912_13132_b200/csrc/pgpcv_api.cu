@@ -164,7 +164,7 @@ struct pgpcv_ctx {
     DevBuf<double> work;
     DevBuf<double> params;
     DevBuf<int2> items;
-    DevBuf<unsigned int> counter;
+    DevBuf<unsigned long long> counter;
     DevBuf<double> subset_loss, subset_nll, sums;  // sums: [loss C | nll C]
     DevBuf<uint8_t> fail;
     DevBuf<int32_t> status;                        // [loss C | nll C]
@@ -180,6 +180,7 @@ struct pgpcv_ctx {
     DevBuf<double> sel_rmspe, sel_local;
     DevBuf<int32_t> sel_best, sel_wins;
     int blocks_per_sm = 0;
+    int sched = 0;  // CvArgs::sched; PGPCV_SCHED overrides (diagnostics)
     pgpcv_timing timing{};
     bool has_timing = false;
 
@@ -444,6 +445,7 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
         return PGPCV_ECUDA;
     }
     ctx->stream = ctx->own_stream;
+    if (const char *env = getenv("PGPCV_SCHED")) ctx->sched = atoi(env);
     for (auto &ev : ctx->ev) cudaEventCreate(&ev);
     if ((e = cv_kernel_occupancy(&ctx->blocks_per_sm)) != cudaSuccess || ctx->blocks_per_sm < 1) {
         g_create_error = std::string("cv kernel cannot be resident: ") + cudaGetErrorString(e);
@@ -699,7 +701,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     }
     CK(ctx->params.ensure(3 * (size_t)L.C), "alloc params");
     CK(ctx->items.ensure(std::max<int64_t>(n_items, 1)), "alloc items");
-    CK(ctx->counter.ensure(1), "alloc counter");
+    CK(ctx->counter.ensure(1 + kMaxSms), "alloc counter");
     // factor workspace: one (k+1) x k factor per resident CTA
     int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_items, 1));
     if (const char *env = getenv("PGPCV_MAX_SLOTS")) {  // diagnostics: cap resident CTAs
@@ -719,7 +721,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     if (n_items)
         CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_items, cudaMemcpyHostToDevice, st),
            "copy items");
-    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned), st), "memset");
+    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * (1 + kMaxSms), st), "memset");
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     if (n_items) {
         CvArgs a;
@@ -736,6 +738,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.items = ctx->items.p;
         a.n_items = (int32_t)n_items;
         a.counter = ctx->counter.p;
+        a.sched = ctx->sched;
         a.work = ctx->work.p;
         a.slot_stride = slot_stride;
         a.out_C = L.out_C;

@@ -21,7 +21,10 @@ struct CvArgs {
     int32_t C;
     const int2 *items;          // [n_items] (subset, config), LPT order
     int32_t n_items;
-    unsigned int *counter;      // dynamic work counter (zeroed before launch)
+    unsigned long long *counter;  // [1 + kMaxSms] zeroed before launch: claims (front | back << 32),
+                                  // then per-SM CTA arrival counts
+    int32_t sched;              // 0: every CTA claims from the front (LPT order); 1: the second
+                                // CTA of each SM claims from the back (smallest k first)
     double *work;               // n_slots * slot_stride doubles: one factor per resident CTA
     size_t slot_stride;
     int32_t out_C;              // output row stride: entry (s, c) at s*out_C + (out_C > 1 ? c : 0)
@@ -36,12 +39,13 @@ struct CvArgs {
     const double *rects;        // [N*4] subset rectangles (the cores)
     double xmax, ymax;          // domain top edges (closed, R3)
     double *gls_out;            // [N * (p+1) * p]: A (p x p row-major) then b (p)
-    unsigned long long *prof;   // [grid * 8] phase cycles (diagnostic build only) or nullptr
+    unsigned long long *prof;   // [grid * 12] phase cycles (diagnostic build only) or nullptr
 };
 constexpr int32_t kCvPredict = 1;  // back-substitution, prediction, SSPE (Eq.3, Eq.4)
 constexpr int32_t kCvNll = 2;      // -2 log-likelihood from the same factor (Eq.2)
 constexpr int32_t kCvGls = 4;      // GLS normal-equation sums from the same factor (Eq. GLS)
 constexpr int32_t kMaxCovariates = 8;
+constexpr int kMaxSms = 256;     // per-SM arrival counters (sched 1)
 
 // Kernel geometry (see cv_kernel.cu for the derivation).
 constexpr int kMT = 128;        // rows per row tile

@@ -282,3 +282,20 @@ def test_partition_device_pointers_match_host(ctx):
     for u, q in zip(a, b):
         assert np.array_equal(u, q)
     assert np.array_equal(ctx.cv_loss(w.params[:2]).subset_loss, la)
+
+
+def test_two_ended_scheduling_is_bit_identical(pg):
+    """PGPCV_SCHED=1 (the second CTA of every SM claims items from the back of the LPT list)
+    changes only which CTA computes which (subset, config): every value is bit-identical."""
+    w = wl("c2")
+    out = []
+    for sched in ("0", "1"):
+        os.environ["PGPCV_SCHED"] = sched
+        try:
+            with pg.Context(0) as c:
+                c.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+                out.append(c.evaluate(w.params, nll=True, subset_nll=True))
+        finally:
+            del os.environ["PGPCV_SCHED"]
+    assert np.array_equal(out[0].subset_loss, out[1].subset_loss)
+    assert np.array_equal(out[0].subset_nll, out[1].subset_nll)
