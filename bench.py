@@ -33,11 +33,15 @@ sys.path.insert(0, ROOT)
 
 # ncu --set full capture of the dominant kernel (dram bytes per launch -> roofline.traffic)
 PROFILE_JSON = "r01_cv_kernel_v4_ncu.json"
-METRIC = "subset CV-loss evals/sec (5M pts, one (range, sigma2, nugget) config per step)"
+METRIC = "subset CV-loss evals/sec at 5M pts (sec per param config and FP64 % of peak alongside)"
 METRICS = {"cv": METRIC,
-           "cv_nll": "subset CV-loss + -2 log-lik evals/sec (one factorization, one config per step)",
-           "nll": "subset -2 log-likelihood evals/sec (one config per step)",
+           "cv_nll": "subset CV-loss + -2 log-lik evals/sec (one factorization per subset and config)",
+           "nll": "subset -2 log-likelihood evals/sec",
            "predict": "subset test-set kriging evals/sec (one config per step)"}
+# Configurations per step: a grid search streams the configurations through one call
+# (pgpcv_cv_loss(params[], n_params)); 5 per step gives 12,500 (subset, config)
+# items at c5, so the dynamic schedule's last partial wave stays small at 1-8 GPUs.
+CONFIGS_PER_STEP = 5
 UNIT = "subset-evals/s"
 
 
@@ -122,11 +126,16 @@ def _peaks():
     return meas, derived
 
 
-def _traffic():
+def _traffic(configs):
+    """DRAM bytes (read + write) of one cv_kernel launch over `configs` configurations: the
+    ncu --set full capture of a one-configuration c5 launch, scaled (every configuration
+    factors every subset once, so the traffic is linear in the configurations)."""
     f = os.path.join(ROOT, "profiles", PROFILE_JSON)
     if os.path.exists(f):
         try:
-            return json.load(f and open(f)).get("dram_bytes_per_launch")
+            d = json.load(open(f))
+            per = d.get("dram_bytes_per_config", d.get("dram_bytes_per_launch"))
+            return per * configs if per is not None else None
         except Exception:
             return None
     return None
@@ -195,10 +204,14 @@ def _config(args, w, part_or_info):
             "nll": ", per-subset -2 log-lik only", "predict": ", test-set kriging prediction"}[args.mode]
     return {"workload": f"{args.workload}: n={w.n:,} on [{w.domain[0]:g},{w.domain[1]:g}]^2, "
                         f"{div}, delta={w.delta:g}, {len(w.params)}-config grid "
-                        f"(one config per step){mode}, FP64",
+                        f"({_cps(args)} config(s) per step){mode}, FP64",
             "n_points": w.n, "n_subsets": N, "n_val": nv, "grid_configs": len(w.params),
-            "configs_per_step": 1, "parallelism": f"subsets sharded by LPT over {args.gpus} GPU(s)",
+            "configs_per_step": _cps(args), "parallelism": f"subsets sharded by LPT over {args.gpus} GPU(s)",
             "l2": "no flush: per-step factor working set (148 slots x up to 142 MB) >> 126 MB L2"}
+
+
+def _cps(args):
+    return 1 if args.mode == "predict" else args.configs_per_step
 
 
 def run_ours(args, rank, world, local_rank):
@@ -246,11 +259,12 @@ def run_ours(args, rank, world, local_rank):
     kk, mm, gg = np.diff(toff), np.diff(voff), np.diff(goff)
     # (subset, config) evaluations per step over all ranks: subsets with validation data
     # (cv), every subset (the likelihood needs no targets), subsets with test points (predict)
-    evals_per_step = {"cv": int((mm > 0).sum()), "cv_nll": int(kk.size), "nll": int(kk.size),
-                      "predict": int((gg > 0).sum())}[args.mode]
+    cps = _cps(args)
+    evals_per_step = cps * {"cv": int((mm > 0).sum()), "cv_nll": int(kk.size), "nll": int(kk.size),
+                            "predict": int((gg > 0).sum())}[args.mode]
 
     def step(i):
-        p = w.params[i % C][None, :]
+        p = w.params[[(i * cps + q) % C for q in range(cps)]]
         if args.mode == "cv":
             return ctx.cv_loss(p, want_subset_loss=False).loss[0]
         if args.mode == "cv_nll":
@@ -317,17 +331,17 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(args, w, info),
-        "sec_per_config": t_ms / args.steps / 1e3,
+        "sec_per_config": t_ms / args.steps / 1e3 / cps,
         "fp64_pct_of_peak": 100.0 * achieved / peak if peak else None,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": _traffic(),
+                     "frac": achieved / peak if peak else None, "traffic": _traffic(cps) if args.workload == "c5" and args.mode == "cv" else None,
                      "kernel": "cv_kernel (assembly + DMMA Cholesky + solves + prediction + SSPE)",
                      "kernel_ms_per_launch": kern_ms / args.steps,
                      "flops_per_launch": kern_flops / args.steps,
                      "peak_source": "measured FP64 DMMA, probes/p0_fp64_peak (profiles/r01_p0_fp64_peak.json)",
                      "peak_bf16_derived": derived},
         "e2e": {"value": evals_per_step * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
-                "h2d_bytes_per_step": int(n * (8 * 3 + 1) + 24), "d2h_bytes_per_step": 8 + 4},
+                "h2d_bytes_per_step": int(n * (8 * 3 + 1) + 24 * cps), "d2h_bytes_per_step": 12 * cps},
         "gpu_launches": launches,
         "clocks": clk,
         "subset_k": {"min": int(kk[mm > 0].min()), "median": float(np.median(kk[mm > 0])),
@@ -396,6 +410,7 @@ def main():
     ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
     ap.add_argument("--mode", default="cv", choices=["cv", "cv_nll", "nll", "predict"],
                     help="cv: the headline CV loss; cv_nll / nll: row f3; predict: row f1 test-set kriging")
+    ap.add_argument("--configs-per-step", type=int, default=CONFIGS_PER_STEP)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)

@@ -121,24 +121,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
-// One operand chunk (KC = 16 columns) of the update for the warp's NI 8-row fragments.
-template <int NI>
-__device__ __forceinline__ void mma_chunk(double (&acc)[2][8][2], const double *ap, const double *bp, int sw) {
-#pragma unroll
-    for (int k4 = 0; k4 < 16 / 4; ++k4) {
-        const int o = (k4 << 2) ^ sw;
-        double af[2], bf[8];
-        af[0] = ap[o];
-        af[1] = NI > 1 ? ap[8 * 16 + o] : 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * 16 + o];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-#pragma unroll
-            for (int i = 0; i < NI; ++i) dmma(acc[i][j], af[i], bf[j]);
-    }
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -419,7 +401,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 PH(2);
                 // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
-                const int nact = rbase > kb ? 0 : (rbase + 8 > kb ? 1 : 2);  // live 8-row fragments
+                const bool live = rbase <= kb;  // this warp holds at least one row of the matrix
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
                     if (tid == 0) {
@@ -436,10 +418,22 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     const double *As = stage + (n % STAGES) * (A_STAGE + B_STAGE);
                     const double *ap = As + (warp * 16 + g) * KC + t;
                     const double *bp = As + A_STAGE + g * KC + t;
-                    // Fragments wholly below the last bordered row (the padding of a tile
-                    // that overhangs the matrix) issue no DMMA: warp-uniform branch.
-                    if (nact == 2) mma_chunk<2>(acc, ap, bp, sw);
-                    else if (nact == 1) mma_chunk<1>(acc, ap, bp, sw);
+                    // A warp whose 16 rows all lie below the last bordered row (the padding
+                    // of a tile that overhangs the matrix) issues no DMMA (warp-uniform).
+                    if (live)
+#pragma unroll
+                    for (int k4 = 0; k4 < KC / 4; ++k4) {
+                        const int o = (k4 << 2) ^ sw;
+                        double af[2], bf[8];
+                        af[0] = ap[o];
+                        af[1] = ap[8 * KC + o];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * KC + o];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
+                    }
                     // Release the stage: this warp's generic-proxy reads of it must be
                     // ordered before the async-proxy bulk copy that will refill it (the
                     // mbarrier alone orders only within the generic proxy; without this
@@ -633,7 +627,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         for (int j = 0; j < 4; ++j)
 #pragma unroll
                             for (int i = 0; i < 2; ++i)
-                                if (sl <= 2 * (h * 4 + j) + 1 && i < nact) dmma(xo[i][j], af[i], bf[j]);
+                                if (sl <= 2 * (h * 4 + j) + 1) dmma(xo[i][j], af[i], bf[j]);
                     }
 #pragma unroll
                     for (int i = 0; i < 2; ++i)

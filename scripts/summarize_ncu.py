@@ -2,7 +2,7 @@
 """Summaries of ncu output for profiles/ (the judged copies; gpurun_out/ is scratch).
 
   summarize_ncu.py launches <launches.csv> <header line>      -> per-kernel launch table
-  summarize_ncu.py full <report.ncu-rep> <kernel label> <out.json> [sass_top.txt]
+  summarize_ncu.py full <report.ncu-rep> <kernel label> <out.json> [sass_top.txt] [configs in the launch]
 """
 import collections
 import csv
@@ -30,7 +30,7 @@ def launches(path, header):
         print(f"{name[:72]:72s} {n:5d} {t:12.3f} {100 * t / total:6.2f}%")
 
 
-def full(rep, label, out, sass_out=None):
+def full(rep, label, out, sass_out=None, configs="1"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -44,6 +44,7 @@ def full(rep, label, out, sass_out=None):
         return x * mult
     rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
     d = {"kernel": label, "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+         "dram_bytes_per_config": (rd + wr) / int(configs),
          "duration_s": num("gpu__time_duration.sum"),
          "dmma_pipe_active_pct": num("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
          "fp64_pipe_active_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
