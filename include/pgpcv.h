@@ -53,9 +53,11 @@ extern "C" {
 #define PGPCV_ENCCL (-7)    /* NCCL unavailable or a collective failed */
 #define PGPCV_ESTATE (-8)   /* cv_loss before partition, or shard after cv_loss */
 
-/* Largest training subset one factorization slot supports (shared-memory bound of the
- * back-substitution; a 19,200-point subset already needs a 2.9 GB factor). */
-#define PGPCV_MAX_K 19200
+/* Largest training subset pgpcv_cv_loss accepts: one resident factorization of k points
+ * holds the packed lower triangle, ~4 k^2 bytes (k = 65,536: 17 GB), and the library
+ * lowers the number of resident factorizations until they fit in device memory
+ * (ENOMEM when even one does not). */
+#define PGPCV_MAX_K 65536
 
 /* Point roles (R7): 0 = training (y_T), 1 = validation (y_V), 2 = test (ignored). */
 #define PGPCV_ROLE_TRAIN 0

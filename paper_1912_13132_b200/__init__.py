@@ -25,7 +25,7 @@ OK, EINVAL, ENUMERIC, EEMPTY, ECUDA, ENOMEM, ENCCL, ESTATE = 0, -2, -3, -4, -5, 
 ERROR_NAMES = {EINVAL: "EINVAL", ENUMERIC: "ENUMERIC", EEMPTY: "EEMPTY", ECUDA: "ECUDA",
                ENOMEM: "ENOMEM", ENCCL: "ENCCL", ESTATE: "ESTATE"}
 NCCL_UNIQUE_ID_BYTES = 128
-MAX_K = 19200
+MAX_K = 65536
 
 # Symbols include/pgpcv.h declares (checked by tests/test_abi.py).
 EXPORTED = ("pgpcv_version", "pgpcv_create", "pgpcv_destroy", "pgpcv_last_error",

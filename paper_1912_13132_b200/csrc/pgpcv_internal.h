@@ -45,7 +45,8 @@ constexpr int32_t kCvPredict = 1;  // back-substitution, prediction, SSPE (Eq.3,
 constexpr int32_t kCvNll = 2;      // -2 log-likelihood from the same factor (Eq.2)
 constexpr int32_t kCvGls = 4;      // GLS normal-equation sums from the same factor (Eq. GLS)
 constexpr int32_t kMaxCovariates = 8;
-constexpr int kMaxSms = 256;     // per-SM arrival counters (sched 1)
+constexpr int kMaxSms = 256;
+#define PGPCV_MAX_K_INTERNAL 65536  // must equal PGPCV_MAX_K in include/pgpcv.h
 
 // Kernel geometry (see cv_kernel.cu for the derivation).
 constexpr int kMT = 128;        // rows per row tile

@@ -1,0 +1,8 @@
+# GPU: pre-generation A/B (default build vs -DPGPCV_NO_PREGEN), tests, phases
+set -x
+timeout 1500 python -m pytest tests -m gpu -x -q -rA --durations=5 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_c5_pregen.json 2> gpurun_out/bench_c5_pregen.err
+PGPCV_LIB=$PWD/probes/libpgpcv_nopregen.so timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_c5_nopregen.json 2> gpurun_out/bench_c5_nopregen.err
+timeout 600 python probes/p2_phases.py c5 > gpurun_out/p2_c5.json 2>&1
+timeout 900 python bench.py --workload c6 --configs-per-step 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c6_cv.json 2> gpurun_out/bench_c6_cv.err
+echo done

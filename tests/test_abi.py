@@ -84,3 +84,10 @@ def test_product_path_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
                 assert "oracle.c" not in txt, f
+
+
+def test_max_k_constant_matches_binding_and_library():
+    src = open(os.path.join(ROOT, "include", "pgpcv.h")).read()
+    hdr = int(re.search(r"#define PGPCV_MAX_K (\d+)", src).group(1))
+    internal = open(os.path.join(ROOT, "paper_1912_13132_b200", "csrc", "pgpcv_internal.h")).read()
+    assert hdr == pg.MAX_K == int(re.search(r"#define PGPCV_MAX_K_INTERNAL (\d+)", internal).group(1))
