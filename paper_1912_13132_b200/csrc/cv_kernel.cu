@@ -350,7 +350,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             __syncwarp();
             __syncthreads();  // cx/cy/cv visible
             PH(1);
-            int ngen = 0;  // entries of this thread's share of the tile pre-generated into L
             for (int rt = 0; rt < ntiles; ++rt) {
                 const int r0 = j0 + rt * MT;
                 const int rbase = r0 + warp * 16;  // this warp's first row
@@ -367,8 +366,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         ry[i] = r < k ? __ldg(ty + r) : 0.0;
                     }
                     // all 32 entries without branches (independent chains the scheduler can
-                    // interleave); the special entries by selects.  Entries the previous
-                    // tile's update loop already generated into L (below) are loaded.
+                    // interleave); the special entries by selects.  (Generating the next
+                    // tile's entries inside the update loop instead was measured 5 % slower:
+                    // the exp chains then compete with the DMMA stream of the same warp.)
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -378,16 +378,12 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 const int r = rbase + i * 8 + g;
                                 const int nl = j * 8 + 2 * t + e;
                                 const int cc = j0 + nl;
-                                if ((i * 8 + j) * 2 + e < ngen && r < k && cc < k) {
-                                    acc[i][j][e] = __ldcg(L + lidx(ld, r, cc));
-                                } else {
-                                    const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
-                                    double v = -exp_neg(sqrt(dx * dx + dy * dy) * ninv, etab);
-                                    v = r == cc ? -(1.0 + lam) : v;                 // exp(0) + lambda
-                                    v = r == k ? -cv[nl] : v;                       // bordered y_T
-                                    v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
-                                    acc[i][j][e] = v;
-                                }
+                                const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
+                                double v = -exp_neg(sqrt(dx * dx + dy * dy) * ninv, etab);
+                                v = r == cc ? -(1.0 + lam) : v;                 // exp(0) + lambda
+                                v = r == k ? -cv[nl] : v;                       // bordered y_T
+                                v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
+                                acc[i][j][e] = v;
                             }
                     if (np > 0) {  // bordered covariate rows (GLS, row f4)
 #pragma unroll
@@ -408,15 +404,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
                 const bool live = rbase <= kb;  // this warp holds at least one row of the matrix
-                // Pre-generation: while its DMMAs run, the warp generates one entry of its
-                // share of the NEXT tile of this block column per operand chunk (entry q =
-                // chunk index, rows < k only) and parks -A there in L (the TRSM overwrites it
-                // later), so the next tile starts with loads instead of exp chains.
-#ifndef PGPCV_NO_PREGEN
-                const int ngen_next = (rt + 1 < ntiles && rbase + MT < k) ? min(nk, 32) : 0;
-#else
-                const int ngen_next = 0;
-#endif
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
                     if (tid == 0) {
@@ -449,14 +436,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 #pragma unroll
                             for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
                     }
-                    if (kc < ngen_next) {
-                        const int i = kc >> 4, nl = ((kc >> 1) & 7) * 8 + 2 * t + (kc & 1);
-                        const int rn = rbase + MT + i * 8 + g, cc = j0 + nl;
-                        if (rn < k && cc < k) {
-                            const double dx = __ldg(tx + rn) - cx[nl], dy = __ldg(ty + rn) - cy[nl];
-                            L[lidx(ld, rn, cc)] = -exp_neg(sqrt(dx * dx + dy * dy) * ninv, etab);
-                        }
-                    }
                     // Release the stage: this warp's generic-proxy reads of it must be
                     // ordered before the async-proxy bulk copy that will refill it (the
                     // mbarrier alone orders only within the generic proxy; without this
@@ -466,7 +445,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     if (lane == 0) mbar_arrive(&empty[n % STAGES]);
                 }
                 pc += nk;
-                ngen = ngen_next;
                 PH(3);
                 // Columns past the matrix (last block column) came from rows of the
                 // workspace beyond the factor: force C = 0 there (Linv^T is 0 there too).
