@@ -148,8 +148,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 // 0 item fetch/setup, 1 block-column setup, 2 A generation, 3 GEMM issue/compute,
 // 4 GEMM operand wait, 5 barrier after tile 0's GEMM, 6 diagonal factorization + inverse,
 // 7 L_jj store + barrier, 8 TRSM + stores, 9 end-of-column fence + barrier,
-// 10 back-substitution, 11 prediction + outputs
-constexpr int kPhases = 12;
+// 10 back-substitution, 11 prediction + outputs; within 6: 12 diagonal setup, 13 panel
+// factorization (warp 0), 14 trailing updates and their barriers
+constexpr int kPhases = 15;
 
 // exp(x) for x <= 0 (x = -d/theta, the exponential covariance), table-driven:
 // x = (64 n + j) ln2/64 + r with |r| <= ln2/128, exp(x) = 2^n * T[j] * (1 + p(r)), T[j] =
@@ -472,14 +473,17 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     }
                     // Blocked Cholesky of C[0:jw, 0:jw] in panels of 8 columns with the inverse
                     // built alongside (R = I - sum L Linv, rows finished panel by panel):
-                    //   warp 0: factor the panel (rsqrt pivots, register shuffles, no CTA
-                    //           barrier) and finish the panel's rows of Linv;
-                    //   all:    trailing update of C and R by the panel (8 FMAs per entry).
+                    //   warp 0:   factor the panel (rsqrt pivots, register shuffles, no CTA
+                    //             barrier) and finish the panel's rows of Linv;
+                    //   warps 1-7, meanwhile: the previous panel's update of the far trailing
+                    //             part of C and R (look-ahead);
+                    //   all:      this panel's update of the next panel's columns and R rows.
                     // 16 CTA barriers per diagonal block instead of 128.
                     double *RI = LJ + NB * LJS;  // R / Linv rows, [n][q] stride LJS
                     for (int e = tid; e < NB * LJS; e += NT) RI[e] = (e / LJS == e % LJS) ? 1.0 : 0.0;
                     if (tid == 0) s_fail = 0;
                     __syncthreads();
+                    PH(12);
                     for (int p0 = 0; p0 < jw; p0 += 8) {
                         const int pw = min(8, jw - p0);
                         if (warp == 0) {
@@ -540,19 +544,44 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 }
                             }
                         }
+                        else if (p0 > 0) {
+                            // Look-ahead: while warp 0 factors this panel, warps 1-7 apply the
+                            // PREVIOUS panel (q0 = p0 - 8) to everything beyond this panel:
+                            // C columns >= f1 and the R rows >= f1.  This panel's own columns
+                            // and R rows got the previous panel in the last iteration's second
+                            // phase, so the two updates touch disjoint entries.
+                            const int q0 = p0 - 8, f1 = p0 + pw, mt = jw - f1;
+                            for (int e = tid - 32; e < mt * mt; e += NT - 32) {
+                                const int rr = f1 + e / mt, cc = f1 + e % mt;
+                                if (cc > rr) continue;
+                                double v = LJ[rr * LJS + cc];
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) v -= LJ[rr * LJS + q0 + i] * LJ[cc * LJS + q0 + i];
+                                LJ[rr * LJS + cc] = v;
+                            }
+                            for (int e = tid - 32; e < mt * p0; e += NT - 32) {
+                                const int rr = f1 + e / p0, q = e % p0;
+                                double v = RI[rr * LJS + q];
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) v -= LJ[rr * LJS + q0 + i] * RI[(q0 + i) * LJS + q];
+                                RI[rr * LJS + q] = v;
+                            }
+                        }
+                        PH(13);
                         __syncthreads();
                         if (s_fail) break;  // uniform
+                        // this panel applied to the NEXT panel's columns and R rows only (all warps)
                         const int p1 = p0 + pw;
                         if (p1 < jw) {
-                            const int mt = jw - p1;
-                            for (int e = tid; e < mt * mt; e += NT) {  // C[rr][cc] -= L[rr][panel] . L[cc][panel]
-                                const int rr = p1 + e / mt, cc = p1 + e % mt;
+                            const int mt = jw - p1, pn = min(8, mt);
+                            for (int e = tid; e < mt * pn; e += NT) {  // C[rr][cc] -= L[rr][panel] . L[cc][panel]
+                                const int rr = p1 + e / pn, cc = p1 + e % pn;
                                 if (cc > rr) continue;
                                 double v = LJ[rr * LJS + cc];
                                 for (int i = 0; i < pw; ++i) v -= LJ[rr * LJS + p0 + i] * LJ[cc * LJS + p0 + i];
                                 LJ[rr * LJS + cc] = v;
                             }
-                            for (int e = tid; e < mt * p1; e += NT) {  // R[rr][q] -= L[rr][panel] . Linv[panel][q]
+                            for (int e = tid; e < pn * p1; e += NT) {  // R[rr][q] -= L[rr][panel] . Linv[panel][q]
                                 const int rr = p1 + e / p1, q = e % p1;
                                 double v = RI[rr * LJS + q];
                                 for (int i = 0; i < pw; ++i) v -= LJ[rr * LJS + p0 + i] * RI[(p0 + i) * LJS + q];
@@ -560,6 +589,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                             }
                         }
                         __syncthreads();
+                        PH(14);
                     }
                     __syncthreads();
                     if (s_fail) {

@@ -755,22 +755,22 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.gls_out = L.gls_out;
         a.prof = nullptr;
 #ifdef PGPCV_PHASE_PROFILE
-        CK(ctx->prof.ensure((size_t)slots * 12), "alloc prof");
-        CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 12, st), "memset");
+        CK(ctx->prof.ensure((size_t)slots * 15), "alloc prof");
+        CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 15, st), "memset");
         a.prof = ctx->prof.p;
 #endif
         CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
 #ifdef PGPCV_PHASE_PROFILE
         {
-            std::vector<unsigned long long> h((size_t)slots * 12);
+            std::vector<unsigned long long> h((size_t)slots * 15);
             CK(cudaMemcpyAsync(h.data(), ctx->prof.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
                                st), "copy prof");
             CK(cudaStreamSynchronize(st), "prof");
-            double sum[12] = {0};
+            double sum[15] = {0};
             for (int b = 0; b < slots; ++b)
-                for (int i = 0; i < 12; ++i) sum[i] += (double)h[(size_t)b * 12 + i];
+                for (int i = 0; i < 15; ++i) sum[i] += (double)h[(size_t)b * 15 + i];
             fprintf(stderr, "PGPCV_PHASES {\"slots\": %d, \"cycles\": [", slots);
-            for (int i = 0; i < 12; ++i) fprintf(stderr, "%s%.6e", i ? ", " : "", sum[i]);
+            for (int i = 0; i < 15; ++i) fprintf(stderr, "%s%.6e", i ? ", " : "", sum[i]);
             fprintf(stderr, "]}\n");
         }
 #endif

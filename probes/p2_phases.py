@@ -10,7 +10,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = ["item_setup", "column_setup", "A_generation", "gemm_issue", "gemm_operand_wait",
          "tile0_barrier", "diag_factor", "diag_store", "trsm_store", "column_end_fence",
-         "back_substitution", "predict_outputs"]
+         "back_substitution", "predict_outputs", "diag_setup", "diag_panel_warp0", "diag_trailing"]
 
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.path.insert(0, ROOT)
