@@ -326,6 +326,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         const int64_t ld = factor_ld(kb);
         const int nblk = (k + NB - 1) / NB;
         const int64_t oi = (int64_t)s * a.out_C + (a.out_C > 1 ? c : 0);  // output entry
+        // slot scratch after the packed factor: alpha (k, when not in SMEM), then the
+        // inverse of every diagonal block (nblk x 64 x 64, row-major) for the solves
+        double *linvG = L + factor_doubles(ld, (k + KC - 1) / KC) + ((k + 31) / 32) * 32;
         bool failed = false;
         double logdet = 0.0;  // sum_i log L_ii (warp 0, kCvNll)
 
@@ -596,10 +599,13 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         failed = true;
                         break;
                     }
-                    // Linv^T for the TRSM-as-GEMM: Bt[q][n] = Linv[n][q] (zero outside the block)
+                    // Linv^T for the TRSM-as-GEMM: Bt[q][n] = Linv[n][q] (zero outside the block);
+                    // Linv itself is kept per block column for the back-substitution.
                     for (int e = tid; e < NB * NB; e += NT) {
                         const int q = e / NB, nn = e % NB;
                         Bt[q * BS + nn] = (q <= nn && nn < jw) ? RI[nn * LJS + q] : 0.0;
+                        const int rr = e / NB, cc2 = e % NB;  // Linv row-major [rr][cc2]
+                        linvG[(size_t)jb * NB * NB + e] = (cc2 <= rr && rr < jw) ? RI[rr * LJS + cc2] : 0.0;
                     }
                     __syncthreads();
                     if ((a.flags & kCvNll) && warp == 0) {  // log det of this diagonal block
@@ -735,7 +741,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         const bool alpha_smem = k + NWARP * NB <= STAGE_DBL;
         double *alpha = alpha_smem ? stage : L + factor_doubles(ld, (k + KC - 1) / KC);
         double *part2 = alpha_smem ? stage + STAGE_DBL - NWARP * NB : stage;
-        double *LB = Bt;        // diagonal block, [row][col] stride LJS
         double *tvec = cx;      // NB
         // L^T alpha = (bordered row rrow): rrow = k gives alpha = (Sigma + lambda I)^{-1} y;
         // rrow = k + 1 + q gives (Sigma + lambda I)^{-1} X[:, q] (GLS).
@@ -762,28 +767,27 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 part2[warp * NB + c0] = p0;
                 part2[warp * NB + c0 + 1] = p1;
             }
-            for (int e = tid; e < jw * jw; e += NT) {
-                const int rr = e / jw, cc = e % jw;  // row rr, column cc of the block
-                if (rr >= cc) LB[rr * LJS + cc] = __ldcg(L + lidx(ld, j0 + rr, j0 + cc));
-            }
             __syncthreads();
             if (tid < jw) {
                 double sum = 0.0;
                 for (int w = 0; w < NWARP; ++w) sum += part2[w * NB + tid];
                 tvec[tid] = __ldcg(L + lidx(ld, rrow, j0 + tid)) - sum;  // z_c - L[c+1:, c] . alpha
-                dg[tid] = 1.0 / LB[tid * LJS + tid];  // reciprocals off the serial sweep below
             }
             __syncthreads();
-            if (warp == 0) {
-                double t0 = lane < jw ? tvec[lane] : 0.0;
-                double t1 = lane + 32 < jw ? tvec[lane + 32] : 0.0;
-                for (int cc = jw - 1; cc >= 0; --cc) {
-                    const double tc = __shfl_sync(0xffffffffu, cc < 32 ? t0 : t1, cc & 31);
-                    const double al = tc * dg[cc];
-                    if (lane < cc) t0 -= LB[cc * LJS + lane] * al;
-                    if (lane + 32 < cc) t1 -= LB[cc * LJS + lane + 32] * al;
-                    if (lane == 0) alpha[j0 + cc] = al;
+            // L_jj^T alpha_j = t  ->  alpha_j = Linv^T t with the block's stored inverse: a
+            // parallel 64 x 64 triangular mat-vec (rows r >= c), coalesced row reads
+            if (tid < jw) {
+                const double *G = linvG + (size_t)jb * NB * NB + tid;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int r = tid;
+                for (; r + 3 < jw; r += 4) {
+                    s0 += __ldcg(G + r * NB) * tvec[r];
+                    s1 += __ldcg(G + (r + 1) * NB) * tvec[r + 1];
+                    s2 += __ldcg(G + (r + 2) * NB) * tvec[r + 2];
+                    s3 += __ldcg(G + (r + 3) * NB) * tvec[r + 3];
                 }
+                for (; r < jw; ++r) s0 += __ldcg(G + r * NB) * tvec[r];
+                alpha[j0 + tid] = (s0 + s1) + (s2 + s3);
             }
             __syncthreads();
         }
@@ -963,7 +967,8 @@ size_t cv_kernel_slot_doubles(int64_t kmax, int extra_rows) {
     // every slot base keeps the alignment bulk copies need.
     const int64_t groups = (kmax + KC - 1) / KC;
     const size_t d = (size_t)factor_doubles(factor_ld(kmax + extra_rows), groups > 0 ? groups : 1) +
-                     (size_t)kmax + (size_t)MT * KC;
+                     (size_t)((kmax + 31) / 32) * 32 + (size_t)((kmax + NB - 1) / NB) * NB * NB +
+                     (size_t)MT * KC;
     return (d + 31) / 32 * 32;
 }
 
