@@ -502,10 +502,24 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                             for (int c2 = 0; c2 < 8; ++c2) {
                                 if (c2 < pw && !bad) {
                                     const double piv = __shfl_sync(0xffffffffu, va[c2], c2);
+                                    // the unscaled column entries of rows p0+c3 do not depend
+                                    // on the pivot: fetched while its rsqrt runs
+                                    double lu[8];
+#pragma unroll
+                                    for (int c3 = c2 + 1; c3 < 8; ++c3) lu[c3] = __shfl_sync(0xffffffffu, va[c2], c3);
                                     if (!(piv > 0.0)) {  // not positive definite (R12); warp-uniform
                                         bad = true;
                                     } else {
                                         const double inv = rsqrt(piv);
+                                        const double rp = inv * inv;  // 1 / pivot
+                                        // trailing columns of the panel with the unscaled column:
+                                        // (u inv)(l inv) = u l / pivot
+#pragma unroll
+                                        for (int c3 = c2 + 1; c3 < 8; ++c3) {
+                                            const double f = lu[c3] * rp;
+                                            va[c3] -= va[c2] * f;
+                                            vb[c3] -= vb[c2] * f;
+                                        }
                                         const double sd = piv * inv;
                                         if (lane == 0) {
                                             dg[p0 + c2] = sd;
@@ -513,12 +527,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                         }
                                         va[c2] = lane == c2 ? sd : (lane > c2 ? va[c2] * inv : va[c2]);
                                         vb[c2] *= inv;
-#pragma unroll
-                                        for (int c3 = c2 + 1; c3 < 8; ++c3) {
-                                            const double l = __shfl_sync(0xffffffffu, va[c2], c3);
-                                            va[c3] -= va[c2] * l;
-                                            vb[c3] -= vb[c2] * l;
-                                        }
                                     }
                                 }
                             }
