@@ -299,3 +299,25 @@ def test_two_ended_scheduling_is_bit_identical(pg):
             del os.environ["PGPCV_SCHED"]
     assert np.array_equal(out[0].subset_loss, out[1].subset_loss)
     assert np.array_equal(out[0].subset_nll, out[1].subset_nll)
+
+
+def test_shard_and_evaluate_argument_rules(ctx, pg):
+    """pgpcv_shard at world 1 owns every subset (same losses); bad rank/world -> EINVAL;
+    shard after an evaluation of the same partition -> ESTATE; an evaluation with no
+    output requested -> EINVAL (include/pgpcv.h)."""
+    w = wl("c1")
+    ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    base = ctx.cv_loss(w.params).subset_loss
+    ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    ctx.shard(0, 1, None)
+    assert np.array_equal(ctx.cv_loss(w.params).subset_loss, base)
+    with pytest.raises(pg.PgpcvError) as ei:
+        ctx.shard(0, 1, None)
+    assert ei.value.code == pg.ESTATE
+    ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    with pytest.raises(pg.PgpcvError) as ei:
+        ctx.shard(1, 1, None)
+    assert ei.value.code == pg.EINVAL
+    with pytest.raises(pg.PgpcvError) as ei:
+        ctx.evaluate(w.params, loss=False, subset_loss=False, nll=False, subset_nll=False)
+    assert ei.value.code == pg.EINVAL
