@@ -33,15 +33,23 @@
 //            3 SMEM stages tracked by full/empty mbarriers (no CTA-wide barrier in the
 //            loop) plus L2 prefetches (cp.async.bulk.prefetch.L2) PFD chunks further ahead
 //   C      = -acc
-//   tile 0 : L_jj = chol(C[0:jw, 0:jw]) and Linv = L_jj^{-1}, fused, in SMEM
+//   tile 0 : L_jj = chol(C[0:jw, 0:jw]) and Linv = L_jj^{-1} in SMEM: 8-column panels
+//            factored by warp 0 (rsqrt pivots, register shuffles), Linv rows finished
+//            per panel, the previous panel's far trailing update by warps 1-7 meanwhile
+//            (look-ahead); 16 CTA barriers per block.  Linv is also kept in the slot.
 //   X      = C . Linv^T                                      -- FP64 DMMA; the A operand
 //            comes straight from the accumulator registers via warp shuffles
 //   L[r0:, j0:j0+jw] = X   (tile 0: its first jw rows are L_jj itself)
+// After the last block column: alpha by blocked back-substitution (warp dot products
+// below each diagonal block + the block's stored inverse), then the prediction.
 //
 // Each warp owns 16 full rows of a tile (8 warps x 16 = 128), so the TRSM needs no
-// cross-warp exchange.  110.7 KB of SMEM and <= 128
-// registers per thread let two CTAs share an SM, so one CTA's barriers, epilogue,
-// diagonal factorization and back-substitution overlap the other's DMMA stream.
+// cross-warp exchange; a warp whose rows all lie in a tile's padding skips the update.
+// ~111 KB of SMEM and <= 128 registers per thread let two CTAs share an SM, so one CTA's
+// barriers, epilogue, diagonal factorization and back-substitution overlap the other's
+// DMMA stream.  The FP64 ALU work outside the update (the covariance's exp/sqrt, the
+// pivots) shares the FP64 pipe with DMMA, so it is kept short: a table-driven exp for
+// x <= 0 and branch-free generation.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
