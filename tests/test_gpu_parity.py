@@ -321,3 +321,32 @@ def test_shard_and_evaluate_argument_rules(ctx, pg):
     with pytest.raises(pg.PgpcvError) as ei:
         ctx.evaluate(w.params, loss=False, subset_loss=False, nll=False, subset_nll=False)
     assert ei.value.code == pg.EINVAL
+
+
+def test_partition_boundary_points_bit_exact(ctx, golden_dir):
+    """The hand-worked golden partition (points on tile edges, on dilated bounds after
+    rounding, the closed domain top, the double just below an edge) and a lattice of points
+    exactly on every tile edge and every dilated bound of a 7 x 5 grid, plus duplicates:
+    GPU membership == the golden lists and == the brute-force oracle bit for bit."""
+    import json
+    g = json.load(open(os.path.join(golden_dir, "partition_small.json")))
+    pts = np.array(g["points"])
+    ctx.partition(pts[:, 0], pts[:, 1], np.ones(len(pts)), pts[:, 2].astype(np.uint8), g["domain"],
+                  g["kx"], g["ky"], g["delta"])
+    toff, tidx, voff, vidx = ctx.partition_export()
+    for s in range(4):
+        assert tidx[toff[s]:toff[s + 1]].tolist() == g["train"][s]
+        assert vidx[voff[s]:voff[s + 1]].tolist() == g["val"][s]
+    D, kx, ky, delta = (0.0, 3.5, -1.0, 1.5), 7, 5, 0.05
+    ex, ey = oracle.edges(D[0], D[1], kx), oracle.edges(D[2], D[3], ky)
+    xs = np.unique(np.clip(np.concatenate([ex, ex - delta, ex + delta, np.nextafter(ex, -np.inf)]), D[0], D[1]))
+    ys = np.unique(np.clip(np.concatenate([ey, ey - delta, ey + delta, np.nextafter(ey, np.inf)]), D[2], D[3]))
+    X, Y = np.meshgrid(xs, ys)
+    x = np.concatenate([X.ravel(), X.ravel()[:50]])  # with duplicates
+    y = np.concatenate([Y.ravel(), Y.ravel()[:50]])
+    role = (np.arange(x.size) % 3 == 1).astype(np.uint8) + (np.arange(x.size) % 7 == 0).astype(np.uint8)
+    ctx.partition(x, y, np.ones(x.size), role, D, kx, ky, delta)
+    toff, tidx, voff, vidx = ctx.partition_export()
+    ref = oracle.partition(x, y, role, D, kx, ky, delta)
+    assert np.array_equal(toff, ref.train_off) and np.array_equal(tidx, ref.train_idx)
+    assert np.array_equal(voff, ref.val_off) and np.array_equal(vidx, ref.val_idx)
