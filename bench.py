@@ -207,7 +207,7 @@ def _config(args, w, part_or_info):
                         f"({_cps(args)} config(s) per step){mode}, FP64",
             "n_points": w.n, "n_subsets": N, "n_val": nv, "grid_configs": len(w.params),
             "configs_per_step": _cps(args), "parallelism": f"subsets sharded by LPT over {args.gpus} GPU(s)",
-            "l2": "no flush: per-step factor working set (148 slots x up to 142 MB) >> 126 MB L2"}
+            "l2": "no flush: per-step factor working set (296 slots x up to 73 MB) >> 126 MB L2"}
 
 
 def _cps(args):
