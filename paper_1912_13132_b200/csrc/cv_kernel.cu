@@ -246,13 +246,13 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
                  "r"((unsigned)(NB * KC * sizeof(double)))
                  : "memory");
 }
-// Tile prologue: SMEM chunks 0..STAGES-1 (every stage) and L2 prefetches of the next PFD.
+// Tile prologue: SMEM chunks 0..STAGES-2 and L2 prefetches of the next PFD chunks.
 __device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage, uint64_t *full,
                                               uint64_t *empty, const double *L, int64_t ld, int r0,
                                               int j0) {
     fence_proxy_async();
-    for (int i = 0; i < min(STAGES, nk); ++i) issue_chunk(pc + i, stage, full, empty, L, ld, r0, j0, i * KC);
-    for (int i = STAGES; i < min(STAGES + PFD, nk); ++i) prefetch_chunk(L, ld, r0, j0, i * KC);
+    for (int i = 0; i < min(STAGES - 1, nk); ++i) issue_chunk(pc + i, stage, full, empty, L, ld, r0, j0, i * KC);
+    for (int i = STAGES - 1; i < min(STAGES - 1 + PFD, nk); ++i) prefetch_chunk(L, ld, r0, j0, i * KC);
 }
 
 __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
@@ -418,6 +418,13 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 const bool live = rbase <= kb;  // this warp holds at least one row of the matrix
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
+                    if (tid == 0) {
+                        if (kc + STAGES - 1 < nk)
+                            issue_chunk(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
+                                        (kc + STAGES - 1) * KC);
+                        if (kc + STAGES - 1 + PFD < nk)
+                            prefetch_chunk(L, ld, r0, j0, (kc + STAGES - 1 + PFD) * KC);
+                    }
                     PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
                     PH(4);
@@ -448,15 +455,6 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[n % STAGES]);
-                    // Refill this chunk's stage with chunk n+STAGES once every warp has
-                    // released it; issued after the producer's own DMMAs for chunk n are
-                    // queued, so waiting for the slowest warp does not hold back its update.
-                    if (tid == 0) {
-                        if (kc + STAGES < nk)
-                            issue_chunk(n + STAGES, stage, full, empty, L, ld, r0, j0, (kc + STAGES) * KC);
-                        if (kc + STAGES + PFD < nk)
-                            prefetch_chunk(L, ld, r0, j0, (kc + STAGES + PFD) * KC);
-                    }
                 }
                 pc += nk;
                 PH(3);
