@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["pgpcv_api.cu", "partition.cu", "cv_kernel.cu", "select.cu", "bisect.cu"]
+SOURCES = ["pgpcv_api.cu", "partition.cu", "cv_kernel.cu", "cv_small.cu", "select.cu", "bisect.cu"]
 LIB = os.path.join(HERE, "libpgpcv.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -25,7 +25,8 @@ def _nccl_include() -> str:
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "pgpcv_internal.h"), os.path.join(ROOT, "include", "pgpcv.h")]
+    deps = srcs + [os.path.join(CSRC, "pgpcv_internal.h"), os.path.join(CSRC, "pgpcv_device.cuh"),
+                   os.path.join(ROOT, "include", "pgpcv.h")]
     lib = out or LIB
     if not force and os.path.exists(lib) and all(os.path.getmtime(lib) >= os.path.getmtime(d) for d in deps):
         return lib

@@ -55,6 +55,7 @@
 #include <cstdint>
 
 #include "pgpcv_internal.h"
+#include "pgpcv_device.cuh"
 
 namespace pgpcv {
 namespace {
@@ -121,19 +122,6 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.global;\n fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// D = A(8x4, row) * B(4x8, col) + D on the FP64 tensor path (SASS DMMA.8x8x4).
-// Fragments: a = A[g][t], b = B[t][g], d = {D[g][2t], D[g][2t+1]} for lane = 4g + t.
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(d[0]), "+d"(d[1])
-        : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
 // Diagnostic build only (-DPGPCV_PHASE_PROFILE, probes/p2_phases.py): thread 0 of every CTA
 // attributes its clock64() time to the phases below; the API prints the sums per launch.
@@ -159,50 +147,6 @@ __device__ __forceinline__ double warp_sum(double v) {
 // 10 back-substitution, 11 prediction + outputs; within 6: 12 diagonal setup, 13 panel
 // factorization (warp 0), 14 trailing updates and their barriers
 constexpr int kPhases = 15;
-
-// exp(x) for x <= 0 (x = -d/theta, the exponential covariance), table-driven:
-// x = (64 n + j) ln2/64 + r with |r| <= ln2/128, exp(x) = 2^n * T[j] * (1 + p(r)), T[j] =
-// 2^(j/64) from SMEM, p the degree-5 Taylor polynomial (truncation r^6/720 < 0.3 ulp).
-// Max error < 1 ulp over [-708, 0] (checked against a 60-digit reference); 10 FP64 ops
-// instead of the ~20 of the general exp().  The FP64 pipe is shared with the co-resident
-// CTA's DMMA stream, so shortening these serial chains shortens the epilogue.
-constexpr int EXP_TAB = 64;
-// 2^(j/64), j = 0..63, correctly rounded (computed to 60 digits; copied to SMEM per CTA)
-__constant__ double kExp2Tab[EXP_TAB] = {
-    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
-    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
-    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
-    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
-    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
-    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
-    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
-    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
-    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
-    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
-    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
-    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
-    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
-    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
-    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
-    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951,
-};
-__device__ __forceinline__ double exp_neg(double x, const double *tab) {
-    const double kShift = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
-    const double t = fma(x, 92.33248261689366, kShift);  // x * 64/ln2 + shift
-    const int ki = __double2loint(t);
-    const double kf = t - kShift;
-    double r = fma(kf, -0.010830424696223417, x);  // ln2/64, high 36 bits
-    r = fma(kf, -2.572804622327669e-14, r);        // ln2/64, low part
-    double p = fma(8.333333333333333e-03, r, 4.1666666666666664e-02);
-    p = fma(p, r, 0.16666666666666666);
-    p = fma(p, r, 0.5);
-    p = fma(p, r, 1.0);
-    p *= r;
-    const double tj = tab[ki & (EXP_TAB - 1)];
-    const double m = fma(tj, p, tj);
-    const double res = __hiloint2double(__double2hiint(m) + ((ki >> 6) << 20), __double2loint(m));
-    return x < -708.0 ? 0.0 : res;
-}
 
 constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));  // 24,576 B
 

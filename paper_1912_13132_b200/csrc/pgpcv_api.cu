@@ -161,7 +161,7 @@ struct pgpcv_ctx {
     std::vector<uint8_t> owned;
 
     // cv_loss buffers
-    DevBuf<double> work;
+    DevBuf<double> work, work_small;
     DevBuf<double> params;
     DevBuf<int2> items;
     DevBuf<unsigned long long> counter;
@@ -179,7 +179,8 @@ struct pgpcv_ctx {
     int32_t sel_C = 0;
     DevBuf<double> sel_rmspe, sel_local;
     DevBuf<int32_t> sel_best, sel_wins;
-    int blocks_per_sm = 0;
+    int blocks_per_sm = 0, blocks_per_sm_small = 0;
+    int small_k = 512;  // items with k <= small_k use cv_small.cu (PGPCV_SMALL_K overrides; 0 disables)
     int sched = 0;  // CvArgs::sched; PGPCV_SCHED overrides (diagnostics)
     pgpcv_timing timing{};
     bool has_timing = false;
@@ -446,7 +447,13 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     }
     ctx->stream = ctx->own_stream;
     if (const char *env = getenv("PGPCV_SCHED")) ctx->sched = atoi(env);
+    if (const char *env = getenv("PGPCV_SMALL_K")) ctx->small_k = atoi(env);
     for (auto &ev : ctx->ev) cudaEventCreate(&ev);
+    if ((e = cv_small_occupancy(&ctx->blocks_per_sm_small)) != cudaSuccess || ctx->blocks_per_sm_small < 1) {
+        g_create_error = std::string("small-subset kernel cannot be resident: ") + cudaGetErrorString(e);
+        pgpcv_destroy(ctx);
+        return PGPCV_ECUDA;
+    }
     if ((e = cv_kernel_occupancy(&ctx->blocks_per_sm)) != cudaSuccess || ctx->blocks_per_sm < 1) {
         g_create_error = std::string("cv kernel cannot be resident: ") + cudaGetErrorString(e);
         pgpcv_destroy(ctx);
@@ -673,6 +680,7 @@ struct CvLaunch {
     const double *gx = nullptr, *gy = nullptr, *gv = nullptr;
     double *subset_loss = nullptr, *subset_nll = nullptr, *yhat = nullptr;
     uint8_t *fail = nullptr;
+    int launches = 0;  // kernel launches run_cv made
     int32_t p = 0;  // GLS covariates (bordered rows below y)
     const double *tX = nullptr;
     double *gls_out = nullptr;
@@ -683,16 +691,24 @@ struct CvLaunch {
 int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     cudaStream_t st = ctx->stream;
     // LPT: descending k (stable, so ties keep ascending subset / config order)
-    std::stable_sort(L.items.begin(), L.items.end(), [&](const int2 &a, const int2 &b) {
-        return ctx->h_train_off[a.x + 1] - ctx->h_train_off[a.x] > ctx->h_train_off[b.x + 1] - ctx->h_train_off[b.x];
-    });
+    auto kof = [&](const int2 &it) { return ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]; };
+    std::stable_sort(L.items.begin(), L.items.end(), [&](const int2 &a, const int2 &b) { return kof(a) > kof(b); });
     int64_t kmax = 0;
-    for (const int2 &it : L.items) kmax = std::max(kmax, ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]);
+    for (const int2 &it : L.items) kmax = std::max(kmax, kof(it));
     if (kmax > cv_kernel_max_k())
         return ctx->fail_with(PGPCV_EINVAL, "a subset has %lld training points (max %d)", (long long)kmax,
                               cv_kernel_max_k());
-    const int64_t n_items = (int64_t)L.items.size();
-    if (n_items >= ((int64_t)1 << 31)) return ctx->fail_with(PGPCV_EINVAL, "too many work items");
+    const int64_t n_all = (int64_t)L.items.size();
+    if (n_all >= ((int64_t)1 << 31)) return ctx->fail_with(PGPCV_EINVAL, "too many work items");
+    // Small subsets go to the warp-per-item kernel (cv_small.cu); the list stays in LPT order,
+    // so the large items are a prefix and the small ones a suffix.
+    const int small_k = (L.flags & kCvGls) ? 0 : std::min(ctx->small_k, kSmallK);
+    int64_t n_big = n_all;
+    while (n_big > 0 && kof(L.items[n_big - 1]) <= small_k) --n_big;
+    const int64_t n_small = n_all - n_big;
+    const int64_t kmax_big = n_big ? kof(L.items[0]) : 0;
+    const int64_t kmax_small = n_small ? kof(L.items[n_big]) : 0;
+
     std::vector<double> hp(3 * (size_t)L.C);
     for (int c = 0; c < L.C; ++c) {
         hp[3 * c] = L.params[c].range;
@@ -700,60 +716,74 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         hp[3 * c + 2] = L.params[c].nugget;
     }
     CK(ctx->params.ensure(3 * (size_t)L.C), "alloc params");
-    CK(ctx->items.ensure(std::max<int64_t>(n_items, 1)), "alloc items");
-    CK(ctx->counter.ensure(1 + kMaxSms), "alloc counter");
-    // factor workspace: one (k+1) x k factor per resident CTA
-    int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_items, 1));
+    CK(ctx->items.ensure(std::max<int64_t>(n_all, 1)), "alloc items");
+    CK(ctx->counter.ensure(2 + kMaxSms), "alloc counter");  // [0] big, [1 .. kMaxSms] SM ranks, [1+kMaxSms] small
+    // factor workspace: one (k+1) x k factor per resident CTA (big) / per warp (small)
+    int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_big, 1));
     if (const char *env = getenv("PGPCV_MAX_SLOTS")) {  // diagnostics: cap resident CTAs
         const int cap = atoi(env);
         if (cap > 0) slots = std::min(slots, cap);
     }
-    const size_t slot_stride = cv_kernel_slot_doubles(kmax, L.p);
-    while (true) {
-        cudaError_t e = ctx->work.ensure((size_t)slots * slot_stride);
-        if (e == cudaSuccess) break;
-        if (slots == 1) return ctx->cuda_fail(e, "alloc factor workspace");
-        slots = std::max(1, slots / 2);
+    const size_t slot_stride = cv_kernel_slot_doubles(kmax_big, L.p);
+    if (n_big) {
+        while (true) {
+            cudaError_t e = ctx->work.ensure((size_t)slots * slot_stride);
+            if (e == cudaSuccess) break;
+            if (slots == 1) return ctx->cuda_fail(e, "alloc factor workspace");
+            slots = std::max(1, slots / 2);
+        }
     }
-    L.slots = slots;
+    const int wpc = cv_small_warps_per_cta();
+    int grid_small = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm_small,
+                                            std::max<int64_t>((n_small + wpc - 1) / wpc, 1));
+    const size_t slot_small = cv_small_slot_doubles(kmax_small);
+    if (n_small) {
+        while (true) {
+            cudaError_t e = ctx->work_small.ensure((size_t)grid_small * wpc * slot_small);
+            if (e == cudaSuccess) break;
+            if (grid_small == 1) return ctx->cuda_fail(e, "alloc small-subset workspace");
+            grid_small = std::max(1, grid_small / 2);
+        }
+    }
+    L.slots = n_big ? slots : grid_small * wpc;
     CK(cudaMemcpyAsync(ctx->params.p, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, st),
        "copy params");
-    if (n_items)
-        CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_items, cudaMemcpyHostToDevice, st),
+    if (n_all)
+        CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_all, cudaMemcpyHostToDevice, st),
            "copy items");
-    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * (1 + kMaxSms), st), "memset");
+    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * (2 + kMaxSms), st), "memset");
     CK(cudaEventRecord(ctx->ev[1], st), "event");
-    if (n_items) {
-        CvArgs a;
-        a.train_off = ctx->train_off.p;
-        a.val_off = L.tgt_off;
-        a.tx = ctx->tx.p;
-        a.ty = ctx->ty.p;
-        a.tv = ctx->tv.p;
-        a.vx = L.gx;
-        a.vy = L.gy;
-        a.vv = L.gv;
-        a.params = ctx->params.p;
-        a.C = L.C;
+    CvArgs a;
+    a.train_off = ctx->train_off.p;
+    a.val_off = L.tgt_off;
+    a.tx = ctx->tx.p;
+    a.ty = ctx->ty.p;
+    a.tv = ctx->tv.p;
+    a.vx = L.gx;
+    a.vy = L.gy;
+    a.vv = L.gv;
+    a.params = ctx->params.p;
+    a.C = L.C;
+    a.sched = ctx->sched;
+    a.out_C = L.out_C;
+    a.flags = L.flags;
+    a.subset_loss = L.subset_loss;
+    a.subset_nll = L.subset_nll;
+    a.yhat = L.yhat;
+    a.fail = L.fail;
+    a.p = L.p;
+    a.tX = L.tX;
+    a.rects = ctx->rects.p;
+    a.xmax = ctx->domain.xmax;
+    a.ymax = ctx->domain.ymax;
+    a.gls_out = L.gls_out;
+    a.prof = nullptr;
+    if (n_big) {
         a.items = ctx->items.p;
-        a.n_items = (int32_t)n_items;
+        a.n_items = (int32_t)n_big;
         a.counter = ctx->counter.p;
-        a.sched = ctx->sched;
         a.work = ctx->work.p;
         a.slot_stride = slot_stride;
-        a.out_C = L.out_C;
-        a.flags = L.flags;
-        a.subset_loss = L.subset_loss;
-        a.subset_nll = L.subset_nll;
-        a.yhat = L.yhat;
-        a.fail = L.fail;
-        a.p = L.p;
-        a.tX = L.tX;
-        a.rects = ctx->rects.p;
-        a.xmax = ctx->domain.xmax;
-        a.ymax = ctx->domain.ymax;
-        a.gls_out = L.gls_out;
-        a.prof = nullptr;
 #ifdef PGPCV_PHASE_PROFILE
         CK(ctx->prof.ensure((size_t)slots * 15), "alloc prof");
         CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 15, st), "memset");
@@ -774,6 +804,17 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
             fprintf(stderr, "]}\n");
         }
 #endif
+        ++L.launches;
+    }
+    if (n_small) {
+        a.items = ctx->items.p + n_big;
+        a.n_items = (int32_t)n_small;
+        a.counter = ctx->counter.p + 1 + kMaxSms;
+        a.work = ctx->work_small.p;
+        a.slot_stride = slot_small;
+        a.prof = nullptr;
+        CK(launch_cv_small(a, grid_small, st), "small-subset kernel launch");
+        ++L.launches;
     }
     CK(cudaEventRecord(ctx->ev[2], st), "event");
     return PGPCV_OK;
@@ -858,7 +899,7 @@ int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, 
     CK(cudaMemsetAsync(ctx->subset_nll.p, 0, sizeof(double) * N * C, st), "memset");
     CK(cudaMemsetAsync(ctx->fail.p, 0, (size_t)N * C, st), "memset");
     if ((rc = run_cv(ctx, L))) return rc;
-    int launches = L.items.empty() ? 0 : 1;
+    int launches = L.launches;
 
     const bool multi = ctx->world > 1;
     const bool gather = multi && (out->subset_loss || out->subset_nll);
@@ -1015,7 +1056,7 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
     CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
     if (yhat) CK(cudaMemsetAsync(ctx->p_yhat.p, 0, sizeof(double) * std::max<int64_t>(n_tgt, 1), st), "memset");
     if ((rc = run_cv(ctx, L))) return rc;
-    int launches = L.items.empty() ? 0 : 1;
+    int launches = L.launches;
     if (ctx->world > 1) {  // exclusive owners: exact sums
         if ((rc = nccl_sum(ctx, ctx->p_sub.p, (size_t)N, ncclFloat64))) return rc;
         if ((rc = nccl_sum(ctx, ctx->p_fail.p, (size_t)N, ncclUint8))) return rc;
@@ -1086,7 +1127,7 @@ int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, dou
     CK(cudaMemsetAsync(ctx->g_part.p, 0, sizeof(double) * N * W, st), "memset");
     CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
     if ((rc = run_cv(ctx, L))) return rc;
-    int launches = 1 + (L.items.empty() ? 0 : 1);
+    int launches = 1 + L.launches;
     if (ctx->world > 1) {  // exclusive owners: exact sums
         if ((rc = nccl_sum(ctx, ctx->g_part.p, (size_t)N * W, ncclFloat64))) return rc;
         if ((rc = nccl_sum(ctx, ctx->p_fail.p, (size_t)N, ncclUint8))) return rc;
