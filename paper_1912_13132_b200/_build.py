@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["pgpcv_api.cu", "partition.cu", "cv_kernel.cu", "cv_small.cu", "select.cu", "bisect.cu"]
+SOURCES = ["pgpcv_api.cu", "partition.cu", "cv_kernel.cu", "select.cu", "bisect.cu"]
 LIB = os.path.join(HERE, "libpgpcv.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -161,7 +161,7 @@ struct pgpcv_ctx {
     std::vector<uint8_t> owned;
 
     // cv_loss buffers
-    DevBuf<double> work, work_small;
+    DevBuf<double> work;
     DevBuf<double> params;
     DevBuf<int2> items;
     DevBuf<unsigned long long> counter;
@@ -179,8 +179,7 @@ struct pgpcv_ctx {
     int32_t sel_C = 0;
     DevBuf<double> sel_rmspe, sel_local;
     DevBuf<int32_t> sel_best, sel_wins;
-    int blocks_per_sm = 0, blocks_per_sm_small = 0;
-    int small_k = 512;  // items with k <= small_k use cv_small.cu (PGPCV_SMALL_K overrides; 0 disables)
+    int blocks_per_sm = 0;
     int sched = 0;  // CvArgs::sched; PGPCV_SCHED overrides (diagnostics)
     pgpcv_timing timing{};
     bool has_timing = false;
@@ -447,13 +446,7 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     }
     ctx->stream = ctx->own_stream;
     if (const char *env = getenv("PGPCV_SCHED")) ctx->sched = atoi(env);
-    if (const char *env = getenv("PGPCV_SMALL_K")) ctx->small_k = atoi(env);
     for (auto &ev : ctx->ev) cudaEventCreate(&ev);
-    if ((e = cv_small_occupancy(&ctx->blocks_per_sm_small)) != cudaSuccess || ctx->blocks_per_sm_small < 1) {
-        g_create_error = std::string("small-subset kernel cannot be resident: ") + cudaGetErrorString(e);
-        pgpcv_destroy(ctx);
-        return PGPCV_ECUDA;
-    }
     if ((e = cv_kernel_occupancy(&ctx->blocks_per_sm)) != cudaSuccess || ctx->blocks_per_sm < 1) {
         g_create_error = std::string("cv kernel cannot be resident: ") + cudaGetErrorString(e);
         pgpcv_destroy(ctx);
@@ -691,24 +684,16 @@ struct CvLaunch {
 int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     cudaStream_t st = ctx->stream;
     // LPT: descending k (stable, so ties keep ascending subset / config order)
-    auto kof = [&](const int2 &it) { return ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]; };
-    std::stable_sort(L.items.begin(), L.items.end(), [&](const int2 &a, const int2 &b) { return kof(a) > kof(b); });
+    std::stable_sort(L.items.begin(), L.items.end(), [&](const int2 &a, const int2 &b) {
+        return ctx->h_train_off[a.x + 1] - ctx->h_train_off[a.x] > ctx->h_train_off[b.x + 1] - ctx->h_train_off[b.x];
+    });
     int64_t kmax = 0;
-    for (const int2 &it : L.items) kmax = std::max(kmax, kof(it));
+    for (const int2 &it : L.items) kmax = std::max(kmax, ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]);
     if (kmax > cv_kernel_max_k())
         return ctx->fail_with(PGPCV_EINVAL, "a subset has %lld training points (max %d)", (long long)kmax,
                               cv_kernel_max_k());
-    const int64_t n_all = (int64_t)L.items.size();
-    if (n_all >= ((int64_t)1 << 31)) return ctx->fail_with(PGPCV_EINVAL, "too many work items");
-    // Small subsets go to the warp-per-item kernel (cv_small.cu); the list stays in LPT order,
-    // so the large items are a prefix and the small ones a suffix.
-    const int small_k = (L.flags & kCvGls) ? 0 : std::min(ctx->small_k, kSmallK);
-    int64_t n_big = n_all;
-    while (n_big > 0 && kof(L.items[n_big - 1]) <= small_k) --n_big;
-    const int64_t n_small = n_all - n_big;
-    const int64_t kmax_big = n_big ? kof(L.items[0]) : 0;
-    const int64_t kmax_small = n_small ? kof(L.items[n_big]) : 0;
-
+    const int64_t n_items = (int64_t)L.items.size();
+    if (n_items >= ((int64_t)1 << 31)) return ctx->fail_with(PGPCV_EINVAL, "too many work items");
     std::vector<double> hp(3 * (size_t)L.C);
     for (int c = 0; c < L.C; ++c) {
         hp[3 * c] = L.params[c].range;
@@ -716,80 +701,67 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         hp[3 * c + 2] = L.params[c].nugget;
     }
     CK(ctx->params.ensure(3 * (size_t)L.C), "alloc params");
-    CK(ctx->items.ensure(std::max<int64_t>(n_all, 1)), "alloc items");
-    CK(ctx->counter.ensure(2 + kMaxSms), "alloc counter");  // [0] big, [1 .. kMaxSms] SM ranks, [1+kMaxSms] small
-    // factor workspace: one (k+1) x k factor per resident CTA (big) / per warp (small)
-    int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_big, 1));
+    CK(ctx->items.ensure(std::max<int64_t>(n_items, 1)), "alloc items");
+    CK(ctx->counter.ensure(1 + kMaxSms), "alloc counter");
+    // factor workspace: one (k+1) x k factor per resident CTA
+    int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_items, 1));
     if (const char *env = getenv("PGPCV_MAX_SLOTS")) {  // diagnostics: cap resident CTAs
         const int cap = atoi(env);
         if (cap > 0) slots = std::min(slots, cap);
     }
-    const size_t slot_stride = cv_kernel_slot_doubles(kmax_big, L.p);
-    if (n_big) {
-        while (true) {
-            cudaError_t e = ctx->work.ensure((size_t)slots * slot_stride);
-            if (e == cudaSuccess) break;
-            if (slots == 1) return ctx->cuda_fail(e, "alloc factor workspace");
-            slots = std::max(1, slots / 2);
-        }
+    const size_t slot_stride = cv_kernel_slot_doubles(kmax, L.p);
+    while (true) {
+        cudaError_t e = ctx->work.ensure((size_t)slots * slot_stride);
+        if (e == cudaSuccess) break;
+        if (slots == 1) return ctx->cuda_fail(e, "alloc factor workspace");
+        slots = std::max(1, slots / 2);
     }
-    const int wpc = cv_small_warps_per_cta();
-    int grid_small = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm_small,
-                                            std::max<int64_t>((n_small + wpc - 1) / wpc, 1));
-    const size_t slot_small = cv_small_slot_doubles(kmax_small);
-    if (n_small) {
-        while (true) {
-            cudaError_t e = ctx->work_small.ensure((size_t)grid_small * wpc * slot_small);
-            if (e == cudaSuccess) break;
-            if (grid_small == 1) return ctx->cuda_fail(e, "alloc small-subset workspace");
-            grid_small = std::max(1, grid_small / 2);
-        }
-    }
-    L.slots = n_big ? slots : grid_small * wpc;
+    L.slots = slots;
     CK(cudaMemcpyAsync(ctx->params.p, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, st),
        "copy params");
-    if (n_all)
-        CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_all, cudaMemcpyHostToDevice, st),
+    if (n_items)
+        CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_items, cudaMemcpyHostToDevice, st),
            "copy items");
-    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * (2 + kMaxSms), st), "memset");
+    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * (1 + kMaxSms), st), "memset");
     CK(cudaEventRecord(ctx->ev[1], st), "event");
-    CvArgs a;
-    a.train_off = ctx->train_off.p;
-    a.val_off = L.tgt_off;
-    a.tx = ctx->tx.p;
-    a.ty = ctx->ty.p;
-    a.tv = ctx->tv.p;
-    a.vx = L.gx;
-    a.vy = L.gy;
-    a.vv = L.gv;
-    a.params = ctx->params.p;
-    a.C = L.C;
-    a.sched = ctx->sched;
-    a.out_C = L.out_C;
-    a.flags = L.flags;
-    a.subset_loss = L.subset_loss;
-    a.subset_nll = L.subset_nll;
-    a.yhat = L.yhat;
-    a.fail = L.fail;
-    a.p = L.p;
-    a.tX = L.tX;
-    a.rects = ctx->rects.p;
-    a.xmax = ctx->domain.xmax;
-    a.ymax = ctx->domain.ymax;
-    a.gls_out = L.gls_out;
-    a.prof = nullptr;
-    if (n_big) {
+    if (n_items) {
+        CvArgs a;
+        a.train_off = ctx->train_off.p;
+        a.val_off = L.tgt_off;
+        a.tx = ctx->tx.p;
+        a.ty = ctx->ty.p;
+        a.tv = ctx->tv.p;
+        a.vx = L.gx;
+        a.vy = L.gy;
+        a.vv = L.gv;
+        a.params = ctx->params.p;
+        a.C = L.C;
         a.items = ctx->items.p;
-        a.n_items = (int32_t)n_big;
+        a.n_items = (int32_t)n_items;
         a.counter = ctx->counter.p;
+        a.sched = ctx->sched;
         a.work = ctx->work.p;
         a.slot_stride = slot_stride;
+        a.out_C = L.out_C;
+        a.flags = L.flags;
+        a.subset_loss = L.subset_loss;
+        a.subset_nll = L.subset_nll;
+        a.yhat = L.yhat;
+        a.fail = L.fail;
+        a.p = L.p;
+        a.tX = L.tX;
+        a.rects = ctx->rects.p;
+        a.xmax = ctx->domain.xmax;
+        a.ymax = ctx->domain.ymax;
+        a.gls_out = L.gls_out;
+        a.prof = nullptr;
 #ifdef PGPCV_PHASE_PROFILE
         CK(ctx->prof.ensure((size_t)slots * 15), "alloc prof");
         CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 15, st), "memset");
         a.prof = ctx->prof.p;
 #endif
         CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
+        ++L.launches;
 #ifdef PGPCV_PHASE_PROFILE
         {
             std::vector<unsigned long long> h((size_t)slots * 15);
@@ -804,17 +776,6 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
             fprintf(stderr, "]}\n");
         }
 #endif
-        ++L.launches;
-    }
-    if (n_small) {
-        a.items = ctx->items.p + n_big;
-        a.n_items = (int32_t)n_small;
-        a.counter = ctx->counter.p + 1 + kMaxSms;
-        a.work = ctx->work_small.p;
-        a.slot_stride = slot_small;
-        a.prof = nullptr;
-        CK(launch_cv_small(a, grid_small, st), "small-subset kernel launch");
-        ++L.launches;
     }
     CK(cudaEventRecord(ctx->ev[2], st), "event");
     return PGPCV_OK;

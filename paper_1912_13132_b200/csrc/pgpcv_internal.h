@@ -60,14 +60,6 @@ __host__ __device__ inline int64_t factor_ld(int64_t k) { return ((k + 1 + 15) /
 
 cudaError_t launch_cv_kernel(const CvArgs &a, int grid, cudaStream_t st);
 
-// Small subsets (cv_small.cu): one warp per (subset, config) item, for k <= kSmallK and
-// without kCvGls.  a.counter's low 32 bits are the claim counter; a.work holds one
-// cv_small_slot_doubles(kmax) slot per warp (grid * cv_small_warps_per_cta() warps).
-constexpr int kSmallK = 640;
-size_t cv_small_slot_doubles(int64_t kmax);
-int cv_small_warps_per_cta();
-cudaError_t cv_small_occupancy(int *blocks_per_sm);
-cudaError_t launch_cv_small(const CvArgs &a, int grid, cudaStream_t st);
 // GLS (row f4): out[w] = sum_s part[s*W + w] in ascending s (W = (p+1) p), then
 // beta = A^{-1} b by Gaussian elimination with partial pivoting; *status = 0 ok, 1 singular.
 cudaError_t launch_gls_solve(const double *part, const uint8_t *fail, int64_t N, int32_t p, double *sums,

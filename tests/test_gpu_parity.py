@@ -350,43 +350,3 @@ def test_partition_boundary_points_bit_exact(ctx, golden_dir):
     ref = oracle.partition(x, y, role, D, kx, ky, delta)
     assert np.array_equal(toff, ref.train_off) and np.array_equal(tidx, ref.train_idx)
     assert np.array_equal(voff, ref.val_off) and np.array_equal(vidx, ref.val_idx)
-
-
-def test_small_subset_kernel_agrees_with_the_block_kernel(pg):
-    """Subsets with k <= 512 run on the warp-per-item kernel (cv_small.cu); with
-    PGPCV_SMALL_K=0 the same items run on the CTA-per-item kernel.  Both within 1e-9 of the
-    oracle elsewhere; here against each other on c2 (CV loss, -2 log L, predictions) and the
-    partial last block around k = 8j (ragged widths 1..7 plus the bordered row inside it)."""
-    w = wl("c2")
-    out = []
-    for sk in ("0", "512"):
-        os.environ["PGPCV_SMALL_K"] = sk
-        try:
-            with pg.Context(0) as c:
-                c.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
-                r = c.evaluate(w.params[::7], nll=True, subset_nll=True)
-                p = c.predict(w.params[3:4], target_role=pg.ROLE_VALIDATION)
-                out.append((r, p))
-        finally:
-            del os.environ["PGPCV_SMALL_K"]
-    (r0, p0), (r1, p1) = out
-    _assert_close(r1.subset_loss, r0.subset_loss, rtol=1e-10)
-    _assert_close(r1.subset_nll, r0.subset_nll, rtol=1e-11)
-    assert np.all(np.abs(p1.yhat - p0.yhat) <= 1e-10 * np.sqrt(np.mean(w.value ** 2)))
-    for k in (1, 7, 8, 9, 15, 17, 63, 64, 65, 511, 512):
-        x, y, v, role = workloads.random_points(4000 + k, k + 5, frac_val=0.0)
-        role[:5] = 1
-        res = []
-        for sk in ("0", "512"):
-            os.environ["PGPCV_SMALL_K"] = sk
-            try:
-                with pg.Context(0) as c:
-                    c.partition(x, y, v, role, (0, 1, 0, 1), 1, 1, 0.0)
-                    res.append(c.evaluate([[0.2, 1.0, 0.1]], nll=True, subset_nll=True))
-            finally:
-                del os.environ["PGPCV_SMALL_K"]
-        _assert_close(res[1].subset_loss, res[0].subset_loss, rtol=1e-10)
-        _assert_close(res[1].subset_nll, res[0].subset_nll, rtol=1e-11)
-        ref_part = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
-        ref = oracle.cv_loss(x, y, v, ref_part, [[0.2, 1.0, 0.1]], threads=2)
-        _assert_close(res[1].subset_loss, ref.subset_loss)
