@@ -37,7 +37,8 @@ METRIC = "subset CV-loss evals/sec at 5M pts (sec per param config and FP64 % of
 METRICS = {"cv": METRIC,
            "cv_nll": "subset CV-loss + -2 log-lik evals/sec (one factorization per subset and config)",
            "nll": "subset -2 log-likelihood evals/sec",
-           "predict": "subset test-set kriging evals/sec (one config per step)"}
+           "predict": "subset test-set kriging evals/sec (one config per step)",
+           "gls": "subset GLS normal-equation evals/sec (covariates 1, x, y; one config per step)"}
 # Configurations per step: a grid search streams the configurations through one call
 # (pgpcv_cv_loss(params[], n_params)); 5 per step gives 12,500 (subset, config)
 # items at c5, so the dynamic schedule's last partial wave stays small at 1-8 GPUs.
@@ -201,7 +202,8 @@ def _config(args, w, part_or_info):
     div = (f"{w.kx}x{w.ky} tiles" if w.depth is None else
            f"recursive bisection into 2^{w.depth} subsets, shell cap {w.shell_cap}")
     mode = {"cv": "", "cv_nll": ", CV loss + per-subset -2 log-lik (one factorization)",
-            "nll": ", per-subset -2 log-lik only", "predict": ", test-set kriging prediction"}[args.mode]
+            "nll": ", per-subset -2 log-lik only", "predict": ", test-set kriging prediction",
+            "gls": ", GLS mean estimate with covariates (1, x, y)"}[args.mode]
     return {"workload": f"{args.workload}: n={w.n:,} on [{w.domain[0]:g},{w.domain[1]:g}]^2, "
                         f"{div}, delta={w.delta:g}, {len(w.params)}-config grid "
                         f"({_cps(args)} config(s) per step){mode}, FP64",
@@ -211,7 +213,7 @@ def _config(args, w, part_or_info):
 
 
 def _cps(args):
-    return 1 if args.mode == "predict" else args.configs_per_step
+    return 1 if args.mode in ("predict", "gls") else args.configs_per_step
 
 
 def run_ours(args, rank, world, local_rank):
@@ -248,6 +250,13 @@ def run_ours(args, rank, world, local_rank):
         return ctx.partition_bisect(hx, hy, hv, hr, w.domain, w.depth, w.delta, w.shell_cap, w.cap_seed)
 
     info = part_device()
+    # Alg.1 lines 2-3 (done once per dataset): timed on a second call (allocations warm)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    info = part_device()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    partition_ms = p0.elapsed_time(p1)
     uid = None
     if world > 1:
         obj = [pg.nccl_unique_id() if rank == 0 else None]
@@ -261,7 +270,10 @@ def run_ours(args, rank, world, local_rank):
     # (cv), every subset (the likelihood needs no targets), subsets with test points (predict)
     cps = _cps(args)
     evals_per_step = cps * {"cv": int((mm > 0).sum()), "cv_nll": int(kk.size), "nll": int(kk.size),
-                            "predict": int((gg > 0).sum())}[args.mode]
+                            "predict": int((gg > 0).sum()), "gls": int((kk > 0).sum())}[args.mode]
+    X = None
+    if args.mode == "gls":  # covariates of the paper's extended model: 1, x, y (scaled)
+        X = np.stack([np.ones(w.n), w.x / w.domain[1], w.y / w.domain[3]], 1)
 
     def step(i):
         p = w.params[[(i * cps + q) % C for q in range(cps)]]
@@ -271,6 +283,8 @@ def run_ours(args, rank, world, local_rank):
             return ctx.evaluate(p, subset_loss=False, nll=True).loss[0]
         if args.mode == "nll":
             return ctx.evaluate(p, loss=False, subset_loss=False, nll=True).nll[0]
+        if args.mode == "gls":
+            return ctx.gls(X, p[0])[0][0]
         return ctx.predict(p, want_yhat=False).sspe
 
     for i in range(args.warmup):
@@ -347,6 +361,7 @@ def run_ours(args, rank, world, local_rank):
         "subset_k": {"min": int(kk[mm > 0].min()), "median": float(np.median(kk[mm > 0])),
                      "max": int(kk.max())},
         "loss_first_step": losses[0],
+        "partition_ms_once_per_dataset": partition_ms,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline(w, args)
@@ -378,6 +393,15 @@ def _oracle_step(w, part, p, sample, cores, mode):
         oracle.cv_loss(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
     if mode in ("cv_nll", "nll"):
         oracle.neg2loglik_all(w.x, w.y, w.value, part, p, subsets=sample, threads=cores)
+    if mode == "gls":
+        import oracle as _o
+        if w.depth is None:
+            ex, ey = _o.edges(w.domain[0], w.domain[1], w.kx), _o.edges(w.domain[2], w.domain[3], w.ky)
+            rects = np.array([[ex[i], ex[i + 1], ey[j], ey[j + 1]] for j in range(w.ky) for i in range(w.kx)])
+        else:
+            rects = part.rects
+        X = np.stack([np.ones(w.n), w.x / w.domain[1], w.y / w.domain[3]], 1)
+        oracle.gls(w.x, w.y, w.value, X, part, rects, w.domain, p[0], subsets=sample, threads=cores)
     if mode == "predict":  # part holds the test lists as its core lists
         sub = oracle.Partition(part.train_off, part.train_idx, part.val_off, part.val_idx, part.n_subsets, 1)
         keep = np.zeros(part.n_subsets, bool)
@@ -434,7 +458,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
-    ap.add_argument("--mode", default="cv", choices=["cv", "cv_nll", "nll", "predict"],
+    ap.add_argument("--mode", default="cv", choices=["cv", "cv_nll", "nll", "predict", "gls"],
                     help="cv: the headline CV loss; cv_nll / nll: row f3; predict: row f1 test-set kriging")
     ap.add_argument("--configs-per-step", type=int, default=CONFIGS_PER_STEP)
     ap.add_argument("--no-cpu-baseline", action="store_true")
