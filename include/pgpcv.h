@@ -283,7 +283,8 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params,
  * core holds the point (R23) -- exact when one subset holds all data.  One
  * factorization per subset serves all p + 1 right-hand sides (bordered rows).
  *   X: host double[n * p], row-major per input point (the n points of the partition call,
- *      in their order); only the training points' rows are used.  1 <= p <= 8.
+ *      in their order); only the training points' rows are used.  1 <= p <= 8.  X is
+ *      not validated: non-finite entries make the affected sums and beta NaN.
  *   param: one configuration (range, sigma2, nugget).
  *   beta: host double[p] out.  xtmx: double[p*p] row-major or NULL; xtmy: double[p] or NULL
  *      (the summed normal equations X^T M^{-1} X, X^T M^{-1} y).
