@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 const int nl = j * 8 + 2 * t + e;
                                 const int cc = j0 + nl;
                                 const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
-                                double v = -exp_neg(sqrt(dx * dx + dy * dy) * ninv, etab);
+                                double v = -exp_neg(sqrt_nb(dx * dx + dy * dy) * ninv, etab);
                                 v = r == cc ? -(1.0 + lam) : v;                 // exp(0) + lambda
                                 v = r == k ? -cv[nl] : v;                       // bordered y_T
                                 v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
