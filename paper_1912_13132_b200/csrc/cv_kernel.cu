@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                     if (!(piv > 0.0)) {  // not positive definite (R12); warp-uniform
                                         bad = true;
                                     } else {
-                                        const double inv = rsqrt(piv);
+                                        const double inv = rsqrt_nb(piv);
                                         const double rp = inv * inv;  // 1 / pivot
                                         // trailing columns of the panel with the unscaled column:
                                         // (u inv)(l inv) = u l / pivot
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             double sum = 0.0;
             for (int j = lane; j < k; j += 32) {
                 const double dx = px - __ldg(tx + j), dy = py - __ldg(ty + j);
-                sum += exp_neg(sqrt(dx * dx + dy * dy) * ninv, etab) * alpha[j];
+                sum += exp_neg(sqrt_nb(dx * dx + dy * dy) * ninv, etab) * alpha[j];
             }
             sum = warp_sum(sum);
             if (a.yhat && lane == 0) a.yhat[voff + v] = sum;
