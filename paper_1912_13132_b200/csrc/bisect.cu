@@ -202,17 +202,19 @@ __global__ void kept_count_kernel(const int64_t *off, const uint8_t *keep, int64
     }
 }
 
-struct Scratch {  // stream-ordered temporaries of one call
+struct Scratch {  // stream-ordered temporaries of one call, from the ctx's own pool
     cudaStream_t st;
+    cudaMemPool_t pool;
     std::vector<void *> ptrs;
-    explicit Scratch(cudaStream_t s) : st(s) {}
+    Scratch(cudaStream_t s, cudaMemPool_t p) : st(s), pool(p) {}
     ~Scratch() {
         for (void *p : ptrs) cudaFreeAsync(p, st);
     }
     template <class T>
     cudaError_t get(T **out, size_t count) {
         void *p = nullptr;
-        cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), st);
+        cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, std::max<size_t>(count, 1) * sizeof(T), pool, st)
+                             : cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), st);
         if (e != cudaSuccess) return e;
         ptrs.push_back(p);
         *out = (T *)p;
@@ -241,8 +243,8 @@ cudaError_t scan_to_host_and_device(const unsigned int *d_cnt, int64_t N, int64_
 
 cudaError_t bisect_tree(int64_t n, const double *x, const double *y, const uint8_t *role, double xmin, double xmax,
                         double ymin, double ymax, int depth, double delta, double *split, double *rect,
-                        cudaStream_t st) {
-    Scratch S(st);
+                        cudaMemPool_t pool, cudaStream_t st) {
+    Scratch S(st, pool);
     const int64_t N = (int64_t)1 << depth;
     double *lvl_rect, *next_rect;
     RET(S.get(&lvl_rect, 4 * N));
@@ -313,8 +315,9 @@ cudaError_t bisect_tree(int64_t n, const double *x, const double *y, const uint8
 
 cudaError_t cap_shells(int64_t N, const int64_t *train_off, const int32_t *train_idx, const double *x,
                        const double *y, const double *rect, double xmax, double ymax, int64_t cap, uint64_t seed,
-                       int32_t *train_idx_out, int64_t *train_off_out, int64_t *n_dropped, cudaStream_t st) {
-    Scratch S(st);
+                       int32_t *train_idx_out, int64_t *train_off_out, int64_t *n_dropped, cudaMemPool_t pool,
+                       cudaStream_t st) {
+    Scratch S(st, pool);
     std::vector<int64_t> hoff(N + 1);
     RET(cudaMemcpyAsync(hoff.data(), train_off, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost, st));
     RET(cudaStreamSynchronize(st));

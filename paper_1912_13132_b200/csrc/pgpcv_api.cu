@@ -131,6 +131,7 @@ struct pgpcv_ctx {
     int sms = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;  // partition scratch; keeps its memory between calls
     std::string err;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -286,7 +287,7 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
         CK(ctx->split.ensure(N), "alloc split");
         CK(ctx->rects.ensure(4 * N), "alloc rects");
         CK(bisect_tree(n, x, y, role, d.xmin, d.xmax, d.ymin, d.ymax, ps.depth, delta, ctx->split.p, ctx->rects.p,
-                       st), "bisection");
+                       ctx->pool, st), "bisection");
         geom.kind = 1;
         geom.tree = Tree{ctx->split.p, ctx->rects.p, ps.depth, d.xmax, d.ymax, delta};
         ctx->h_rects.resize(4 * N);
@@ -357,7 +358,7 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
         CK(ctx->train_idx2.ensure(std::max<int64_t>(sum_k, 1)), "alloc");
         CK(ctx->train_off2.ensure(N + 1), "alloc");
         CK(cap_shells(N, ctx->train_off.p, ctx->train_idx.p, x, y, ctx->rects.p, d.xmax, d.ymax, ps.shell_cap,
-                      ps.seed, ctx->train_idx2.p, ctx->train_off2.p, &dropped, st), "shell cap");
+                      ps.seed, ctx->train_idx2.p, ctx->train_off2.p, &dropped, ctx->pool, st), "shell cap");
         ctx->train_idx.swap(ctx->train_idx2);
         ctx->train_off.swap(ctx->train_off2);
         CK(cudaMemcpyAsync(ctx->h_train_off.data(), ctx->train_off.p, sizeof(int64_t) * (N + 1),
@@ -445,6 +446,19 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
         return PGPCV_ECUDA;
     }
     ctx->stream = ctx->own_stream;
+    {  // a private stream-ordered pool that never returns memory at synchronisation
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = cuda_device;
+        if (cudaMemPoolCreate(&ctx->pool, &props) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        } else {
+            ctx->pool = nullptr;  // fall back to the device's default pool
+            cudaGetLastError();
+        }
+    }
     if (const char *env = getenv("PGPCV_SCHED")) ctx->sched = atoi(env);
     for (auto &ev : ctx->ev) cudaEventCreate(&ev);
     if ((e = cv_kernel_occupancy(&ctx->blocks_per_sm)) != cudaSuccess || ctx->blocks_per_sm < 1) {
@@ -464,6 +478,7 @@ void pgpcv_destroy(pgpcv_ctx *ctx) {
     for (auto &ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
 }
 

@@ -171,16 +171,17 @@ cudaError_t launch_gather(int64_t cnt, const int32_t *idx, const double *x, cons
 // ----------------------------------------------------------------------------------------
 // Computes split[1 .. 2^depth - 1] and the leaf rectangles rect[2^depth * 4] (device
 // arrays, caller-allocated) for points with role <= 1, level by level; scratch comes from
-// the stream-ordered allocator.  Synchronises `st` once per level.
+// `pool` (stream-ordered; the ctx keeps it across calls).  Synchronises `st` once per level.
 cudaError_t bisect_tree(int64_t n, const double *x, const double *y, const uint8_t *role, double xmin,
                         double xmax, double ymin, double ymax, int depth, double delta, double *split,
-                        double *rect, cudaStream_t st);
+                        double *rect, cudaMemPool_t pool, cudaStream_t st);
 // Shell cap (R22) on CSR training lists (ascending index) of N subsets with rectangles
 // rect (device arrays): writes the capped lists (ascending index) to train_idx_out /
 // train_off_out (device, capacity sum_k / N+1) and the number of dropped members to
 // *n_dropped (host).  Synchronises `st`.
 cudaError_t cap_shells(int64_t N, const int64_t *train_off, const int32_t *train_idx, const double *x,
                        const double *y, const double *rect, double xmax, double ymax, int64_t cap, uint64_t seed,
-                       int32_t *train_idx_out, int64_t *train_off_out, int64_t *n_dropped, cudaStream_t st);
+                       int32_t *train_idx_out, int64_t *train_off_out, int64_t *n_dropped, cudaMemPool_t pool,
+                       cudaStream_t st);
 
 }  // namespace pgpcv
