@@ -32,6 +32,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
 
 wname = sys.argv[1] if len(sys.argv) > 1 else "c5"
 lib = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "paper_1912_13132_b200", "libpgpcv_phases.so")
+if not os.path.exists(lib):  # the diagnostic build (not part of __graft_entry__.build())
+    sys.path.insert(0, ROOT)
+    from paper_1912_13132_b200 import _build
+    _build.build(force=True, defines=["PGPCV_PHASE_PROFILE"], out=lib)
 env = dict(os.environ, PGPCV_LIB=lib)
 r = subprocess.run([sys.executable, __file__, "child", wname], env=env, capture_output=True, text=True)
 m = re.search(r"PGPCV_PHASES (\{.*\})", r.stderr)
