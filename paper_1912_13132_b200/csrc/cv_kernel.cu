@@ -118,22 +118,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-#ifndef PGPCV_NO_L2_HINTS
-// Same copy with an L2 eviction-priority policy (createpolicy): the 64-row B panel of a block
-// column is re-read by every row tile of the column (keep: evict_last), the 128-row A
-// chunk is read once per block column (evict_first).
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, unsigned bytes, uint64_t *bar,
-                                              bool keep) {
-    uint64_t pol;
-    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-#endif
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.global;\n fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -195,13 +179,8 @@ __device__ __forceinline__ void issue_chunk(uint32_t n, double *stage, uint64_t 
     if (use > 0) mbar_wait(&empty[sidx], (use - 1) & 1);
     double *sb = stage + sidx * (A_STAGE + B_STAGE);
     mbar_expect_tx(&full[sidx], STAGE_BYTES);
-#ifndef PGPCV_NO_L2_HINTS
-    bulk_g2s_hint(sb, lchunk(L, ld, kk / KC, r0), MT * KC * sizeof(double), &full[sidx], false);
-    bulk_g2s_hint(sb + A_STAGE, lchunk(L, ld, kk / KC, j0), NB * KC * sizeof(double), &full[sidx], true);
-#else
     bulk_g2s(sb, lchunk(L, ld, kk / KC, r0), MT * KC * sizeof(double), &full[sidx]);
     bulk_g2s(sb + A_STAGE, lchunk(L, ld, kk / KC, j0), NB * KC * sizeof(double), &full[sidx]);
-#endif
 }
 __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int r0, int j0, int kk) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lchunk(L, ld, kk / KC, r0)),
