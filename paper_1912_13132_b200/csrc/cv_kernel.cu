@@ -126,12 +126,32 @@ __device__ __forceinline__ void fence_proxy_async() {
 // Diagnostic build only (-DPGPCV_PHASE_PROFILE, probes/p2_phases.py): thread 0 of every CTA
 // attributes its clock64() time to the phases below; the API prints the sums per launch.
 #ifdef PGPCV_PHASE_PROFILE
-#define PH_DECL long long ph_t = clock64();
+#ifdef PGPCV_TIMELINE
+// Timeline (probes/p3_timeline.py): thread 0 logs the SM clock each time its CTA switches
+// between the update (phases 3-4) and anything else; word 0 of a CTA's log is its SM id.
+constexpr int kTimelineLen = 1 << 15;
+#define TL_LOG(i, t0)                                                                        \
+    do {                                                                                     \
+        const int st_ = ((i) == 3 || (i) == 4) ? 1 : 0;                                      \
+        if (st_ != tl_state && a.tl && tl_n < kTimelineLen - 2) {                            \
+            a.tl[(size_t)blockIdx.x * kTimelineLen + 2 + tl_n++] = ((unsigned long long)(t0) << 1) | st_; \
+            tl_state = st_;                                                                  \
+        }                                                                                    \
+    } while (0)
+#define TL_DECL int tl_state = -1, tl_n = 0;
+#else
+#define TL_LOG(i, t0) \
+    do {              \
+    } while (0)
+#define TL_DECL
+#endif
+#define PH_DECL long long ph_t = clock64(); TL_DECL
 #define PH(i)                                   \
     do {                                        \
         if (tid == 0) {                         \
             const long long t_ = clock64();     \
             s_ph[i] += (unsigned long long)(t_ - ph_t); \
+            TL_LOG(i, ph_t);                    \
             ph_t = t_;                          \
         }                                       \
     } while (0)
@@ -259,6 +279,14 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 #ifdef PGPCV_PHASE_PROFILE
             PH(0);
             if (tid < kPhases && a.prof) a.prof[blockIdx.x * kPhases + tid] = s_ph[tid];
+#ifdef PGPCV_TIMELINE
+            if (tid == 0 && a.tl) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                a.tl[(size_t)blockIdx.x * kTimelineLen] = smid;
+                a.tl[(size_t)blockIdx.x * kTimelineLen + 1] = (unsigned long long)tl_n;
+            }
+#endif
 #endif
             break;
         }

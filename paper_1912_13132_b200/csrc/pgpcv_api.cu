@@ -176,6 +176,7 @@ struct pgpcv_ctx {
     // pgpcv_gls
     DevBuf<double> g_X, g_tX, g_part, g_sums, g_beta;
     DevBuf<unsigned long long> prof;  // diagnostic phase cycles (-DPGPCV_PHASE_PROFILE)
+    DevBuf<unsigned long long> tl;    // diagnostic timeline (-DPGPCV_TIMELINE)
     // pgpcv_select: the last evaluation's device-resident per-subset losses
     int32_t sel_C = 0;
     DevBuf<double> sel_rmspe, sel_local;
@@ -775,7 +776,25 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 15, st), "memset");
         a.prof = ctx->prof.p;
 #endif
+        a.tl = nullptr;
+#ifdef PGPCV_TIMELINE
+        CK(ctx->tl.ensure((size_t)slots * 32768), "alloc timeline");
+        CK(cudaMemsetAsync(ctx->tl.p, 0, sizeof(unsigned long long) * slots * 32768, st), "memset");
+        a.tl = ctx->tl.p;
+#endif
         CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
+#ifdef PGPCV_TIMELINE
+        if (const char *path = getenv("PGPCV_TIMELINE_FILE")) {
+            std::vector<unsigned long long> h((size_t)slots * 32768);
+            CK(cudaMemcpyAsync(h.data(), ctx->tl.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
+                               st), "copy timeline");
+            CK(cudaStreamSynchronize(st), "timeline");
+            if (FILE *f = fopen(path, "wb")) {
+                fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+                fclose(f);
+            }
+        }
+#endif
         ++L.launches;
 #ifdef PGPCV_PHASE_PROFILE
         {

@@ -40,6 +40,7 @@ struct CvArgs {
     double xmax, ymax;          // domain top edges (closed, R3)
     double *gls_out;            // [N * (p+1) * p]: A (p x p row-major) then b (p)
     unsigned long long *prof;   // [grid * 15] phase cycles (diagnostic build only) or nullptr
+    unsigned long long *tl;     // [grid * 32768] GEMM/non-GEMM timeline (diagnostic) or nullptr
 };
 constexpr int32_t kCvPredict = 1;  // back-substitution, prediction, SSPE (Eq.3, Eq.4)
 constexpr int32_t kCvNll = 2;      // -2 log-likelihood from the same factor (Eq.2)
