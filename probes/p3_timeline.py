@@ -42,7 +42,7 @@ for cta, row in enumerate(raw):
     if n < 4:
         continue
     ev = row[2:2 + n]
-    by_sm.setdefault(int(row[0]), []).append((ev >> np.uint64(1)).astype(np.int64), (ev & np.uint64(1)).astype(np.int8))
+    by_sm.setdefault(int(row[0]), []).append(((ev >> np.uint64(1)).astype(np.int64), (ev & np.uint64(1)).astype(np.int8)))
 stats = []
 for sm, ctas in sorted(by_sm.items()):
     if len(ctas) != 2:
