@@ -228,8 +228,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
     double *cy = cx + NB;
     double *cv = cy + NB;
     double *dg = cv + NB;               // sqrt pivots of the diagonal block
-    double *rdg = dg + NB;              // reciprocal pivots
-    double *red = rdg + NB;             // per-warp partial sums
+    double *red = dg + 2 * NB;          // per-warp partial sums
     double *etab = red + NWARP;         // 2^(j/64), j = 0..63 (exp_neg)
     __shared__ __align__(8) uint64_t full[STAGES];
     __shared__ __align__(8) uint64_t empty[STAGES];
@@ -478,6 +477,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                 vb[c2] = (rb < jw && c2 < pw) ? LJ[rb * LJS + p0 + c2] : 0.0;
                             }
                             bool bad = false;
+                            double rinv[8];
+#pragma unroll
+                            for (int c2 = 0; c2 < 8; ++c2) rinv[c2] = 0.0;
 #pragma unroll
                             for (int c2 = 0; c2 < 8; ++c2) {
                                 if (c2 < pw && !bad) {
@@ -501,10 +503,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                                             vb[c3] -= vb[c2] * f;
                                         }
                                         const double sd = piv * inv;
-                                        if (lane == 0) {
-                                            dg[p0 + c2] = sd;
-                                            rdg[p0 + c2] = inv;
-                                        }
+                                        rinv[c2] = inv;
+                                        if (lane == 0) dg[p0 + c2] = sd;
                                         va[c2] = lane == c2 ? sd : (lane > c2 ? va[c2] * inv : va[c2]);
                                         vb[c2] *= inv;
                                     }
@@ -517,21 +517,32 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                             }
                             if (bad && lane == 0) s_fail = 1;
                             __syncwarp();
-                            // the panel's rows of Linv: Linv[r] = (R[r] - sum_{i2<i} L[r][p0+i2] Linv[p0+i2]) / L[r][r]
+                            // the panel's rows of Linv: Linv[r] = (R[r] - sum_{i2<i} L[r][p0+i2] Linv[p0+i2]) / L[r][r],
+                            // a forward substitution in registers: lane owns columns q = lane, lane + 32
+                            // of the panel's 8 rows; L[p0+i][p0+i2] comes from lane i's va[i2]
+                            // (entries with q > r stay exactly 0, as Linv is lower triangular)
                             if (!bad) {
-                                for (int i = 0; i < pw; ++i) {
-                                    const int r = p0 + i;
+                                double w0[8], w1[8];
 #pragma unroll
-                                    for (int h = 0; h < 2; ++h) {
-                                        const int q = lane + 32 * h;
-                                        if (q <= r) {
-                                            double v = RI[r * LJS + q];
-                                            for (int i2 = 0; i2 < i; ++i2)
-                                                v -= LJ[r * LJS + p0 + i2] * RI[(p0 + i2) * LJS + q];
-                                            RI[r * LJS + q] = v * rdg[r];
-                                        }
+                                for (int i = 0; i < 8; ++i) {
+                                    w0[i] = i < pw ? RI[(p0 + i) * LJS + lane] : 0.0;
+                                    w1[i] = i < pw ? RI[(p0 + i) * LJS + lane + 32] : 0.0;
+                                }
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+#pragma unroll
+                                    for (int i2 = 0; i2 < i; ++i2) {
+                                        const double l = __shfl_sync(0xffffffffu, va[i2], i);
+                                        w0[i] -= l * w0[i2];
+                                        w1[i] -= l * w1[i2];
                                     }
-                                    __syncwarp();
+                                    w0[i] = lane <= p0 + i ? w0[i] * rinv[i] : 0.0;
+                                    w1[i] = lane + 32 <= p0 + i ? w1[i] * rinv[i] : 0.0;
+                                }
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    if (i < pw && lane <= p0 + i) RI[(p0 + i) * LJS + lane] = w0[i];
+                                    if (i < pw && lane + 32 <= p0 + i) RI[(p0 + i) * LJS + lane + 32] = w1[i];
                                 }
                             }
                         }
