@@ -162,10 +162,13 @@ def test_c5_full_size_sampled(ctx):
     assert 0.3 < rmspe < 0.5
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 31, 63, 64, 65, 127, 128, 129, 255, 257, 700])
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8, 9, 31, 33, 40, 63, 64, 65, 71, 100, 127, 128, 129,
+                               200, 255, 257, 700])
 def test_ragged_single_subset(ctx, k):
     """One tile (Eq.7 with N = 1 is Eq.4): k training points not a multiple of the 64-wide
-    block or the 128-row tile, m = 7 validation points."""
+    block or the 128-row tile, m = 7 validation points. The diagonal block's 8-column
+    panels see partial (5, 9, 71: a 7-wide last block) and exact (8, 40) widths, rows
+    beyond lane 32 of warp 0 (33, 40, 100) and the panels from column 32 on (40, 100, 200)."""
     m = 7
     rng = np.random.default_rng(1000 + k)
     n = k + m
