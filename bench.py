@@ -3,16 +3,21 @@
 sec per parameter configuration at 5M points; FP64 % of peak).
 
 A "step" is one pass of the whole hot path (Alg.1 lines 4-9) over all
-2,500 subsets of the 5M-point workload c5 for ONE (range, sigma2, nugget) configuration of
-its 125-point grid (steps cycle through the grid): covariance assembly, FP64 Cholesky,
-solves, prediction, loss reduction (and the NCCL all-reduce when N > 1).  The partition
-(Alg.1 lines 2-3, "done once") happens before the timed region for `value`, and
-inside every step for `e2e` (host arrays -> C ABI -> host loss).
+2,500 subsets of the 5M-point workload c5 for a batch of `--configs-per-step` (default 5)
+(range, sigma2, nugget) configurations of its 125-point grid (steps walk through the grid):
+covariance assembly, FP64 Cholesky, solves, prediction, loss reduction (and the NCCL
+combine when N > 1).  `--configs-per-step 125` streams the whole grid through one call
+(bit-identical (range, lambda) pairs are then factored once; `configs_executed`).
+The partition (Alg.1 lines 2-3, "done once") happens before the timed region for
+`value`, and inside every step for `e2e` (host arrays -> C ABI -> host loss).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1..c6] [--mode cv|cv_nll|nll|predict|gls]
 
-N > 1 is launched by torchrun (one rank per GPU); times are CUDA-event times, max over
-ranks.  `--impl reference` times the CPU oracle (the reference arm of this tier) on rank 0.
+N > 1: launched by torchrun (one rank per GPU), or, without WORLD_SIZE in the environment,
+bench.py launches torchrun itself; times are CUDA-event times, max over ranks.
+`--impl reference` times the CPU oracle (the reference arm of this tier) on rank 0.
+`--dry-run` exercises the multi-rank launch and combine on CPU (gloo, no GPU).
 """
 from __future__ import annotations
 
@@ -52,7 +57,9 @@ def _env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region,
+    plus one synchronous snapshot when it starts and one when it stops (so a timed region
+    shorter than the sampling period still has a clock record)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -64,7 +71,16 @@ class ClockSampler:
         self.lines = []
         self.thread = None
 
+    def _snapshot(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+            self.lines.extend(ln.strip() for ln in out.stdout.splitlines() if ln.strip())
+        except (OSError, subprocess.TimeoutExpired):
+            pass
+
     def start(self):
+        self._snapshot()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -83,6 +99,7 @@ class ClockSampler:
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self._snapshot()
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -208,7 +225,8 @@ def _config(args, w, part_or_info):
                         f"{div}, delta={w.delta:g}, {len(w.params)}-config grid "
                         f"({_cps(args)} config(s) per step){mode}, FP64",
             "n_points": w.n, "n_subsets": N, "n_val": nv, "grid_configs": len(w.params),
-            "configs_per_step": _cps(args), "parallelism": f"subsets sharded by LPT over {args.gpus} GPU(s)",
+            "configs_per_step": _cps(args),
+            "parallelism": f"whole subsets sharded by LPT on k^3 over {args.gpus} GPU(s), one rank per GPU",
             "l2": "no flush: per-step factor working set (296 slots x up to 73 MB) >> 126 MB L2"}
 
 
@@ -300,7 +318,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kern_ms, kern_flops, launches, losses = 0.0, 0.0, 0, []
+    kern_ms, kern_flops, launches, losses, executed = 0.0, 0.0, 0, [], 0
     e0.record(stream)
     for i in range(args.steps):
         r = step(args.warmup + i)
@@ -308,6 +326,7 @@ def run_ours(args, rank, world, local_rank):
         kern_ms += t["kernel_ms"]
         kern_flops += t["flops"]
         launches += t["launches"]
+        executed += t["n_configs_executed"]
         losses.append(float(r))
     e1.record(stream)
     barrier()
@@ -346,9 +365,11 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(args, w, info),
         "sec_per_config": t_ms / args.steps / 1e3 / cps,
+        "configs_per_step": cps,
+        "configs_executed_per_step": executed / args.steps,
         "fp64_pct_of_peak": 100.0 * achieved / peak if peak else None,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": _traffic(cps) if args.workload == "c5" and args.mode == "cv" else None,
+                     "frac": achieved / peak if peak else None, "traffic": _traffic(executed / args.steps) if args.workload == "c5" and args.mode == "cv" else None,
                      "kernel": "cv_kernel (assembly + DMMA Cholesky + solves + prediction + SSPE)",
                      "kernel_ms_per_launch": kern_ms / args.steps,
                      "flops_per_launch": kern_flops / args.steps,
@@ -363,6 +384,8 @@ def run_ours(args, rank, world, local_rank):
         "loss_first_step": losses[0],
         "partition_ms_once_per_dataset": partition_ms,
     }
+    if world > 1:
+        line["nccl_library"] = pg.nccl_library()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline(w, args)
     if rank == 0:
@@ -451,6 +474,51 @@ def _lapack_baseline(w, part, sample, prm):
             "seconds": dt}
 
 
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """--gpus N without a torchrun environment: run this script under torchrun, one rank
+    per GPU on this node (rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world, local_rank):
+    """Multi-rank plumbing without a GPU: gloo process group, the library's LPT ownership
+    rule over c5-sized synthetic subsets, the max-over-ranks timing reduction; rank 0 prints
+    one JSON line naming every rank it saw."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_13132_b200 as pg
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    k = np.random.default_rng(0).integers(2600, 4300, 2500).astype(np.float64)
+    owner = pg.lpt_assign(k ** 3, world)
+    mine = int((owner == rank).sum())
+    me = torch.tensor([rank, local_rank, world, os.getpid(), mine], dtype=torch.float64)
+    rows = [me.clone() for _ in range(world)]
+    if world > 1:
+        dist.all_gather(rows, me)
+        t = torch.tensor([float(rank + 1)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_requested": args.gpus,
+                          "ranks": [[int(v) for v in r.tolist()] for r in rows],
+                          "subsets_per_rank": [int(r[4]) for r in rows]}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -462,12 +530,27 @@ def main():
                     help="cv: the headline CV loss; cv_nll / nll: row f3; predict: row f1 test-set kriging")
     ap.add_argument("--configs-per-step", type=int, default=CONFIGS_PER_STEP)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank launch/combine on CPU (gloo), no GPU")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return launch_ranks(args)
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
     local_rank = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to run", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return run_dry(args, rank, world, local_rank)
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    import torch
+    if torch.cuda.device_count() < world:
+        print(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s); refusing to run",
+              file=sys.stderr)
+        return 2
     return run_ours(args, rank, world, local_rank)
 
 

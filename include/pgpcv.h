@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PGPCV_VERSION 4
+#define PGPCV_VERSION 5
 
 /* Error codes. */
 #define PGPCV_OK 0
@@ -114,6 +114,9 @@ typedef struct {
     int64_t n_evals;      /* (subset, config) evaluations this rank executed (m > 0 only) */
     int32_t launches;     /* number of libpgpcv kernel launches in the call */
     int32_t n_slots;      /* resident CTAs (factorization slots) of the dominant kernel */
+    int32_t n_configs_executed; /* configurations factored: pgpcv_evaluate factors each
+                                   bit-identical (range, lambda) pair once */
+    int32_t reserved;
 } pgpcv_timing;
 
 /* Library version (PGPCV_VERSION).  Never fails; needs no GPU. */
@@ -205,11 +208,30 @@ int pgpcv_partition_export(pgpcv_ctx *ctx, int64_t *train_off, int32_t *train_id
 /* Multi-GPU (Alg.1's parfor over subsets, across the GPUs of one box).
  * rank in [0, world); world >= 1.  nccl_unique_id: NCCL_UNIQUE_ID_BYTES (128) bytes from
  * pgpcv_nccl_get_unique_id on rank 0, broadcast by the caller; ignored (may be NULL) when
- * world == 1.  Creates the NCCL communicator and assigns whole subsets to ranks by LPT on
- * the cost k_s^3 (ties by subset id), identically on every rank.  Must be called after
- * pgpcv_partition and before the first pgpcv_cv_loss of that partition (else ESTATE);
- * without it a ctx owns every subset.  Errors: EINVAL, ESTATE, ENCCL. */
+ * world == 1.  Creates the NCCL communicator (collective over the `world` ranks).  Every
+ * later evaluation assigns the whole subsets it factors to ranks by LPT on the cost k_s^3
+ * (pgpcv_lpt_assign; ties by subset id), identically on every rank, and combines the
+ * results with NCCL all-reduces.  Must be called after pgpcv_partition and before the
+ * first evaluation of that partition (else ESTATE), or again after a collective failed.
+ * Without it a ctx owns every subset.  The sharding stays in effect for later partitions of
+ * the same ctx (each rank must then partition the same data).  On any error the ctx is
+ * left at rank 0 of world 1
+ * (no communicator).  Errors: EINVAL (bad rank/world, world > 1 without an id), ESTATE,
+ * ENCCL (libnccl not loadable, ncclCommInitRank failed).
+ *
+ * Failure behaviour at world > 1: every rank-local failure (allocation, launch) is agreed
+ * on by all ranks (one MAX all-reduce of an error flag) before any data collective, so
+ * peers return ENCCL instead of blocking.  While waiting on a collective the library polls
+ * ncclCommGetAsyncError; an NCCL error, or no completion within PGPCV_NCCL_TIMEOUT_S
+ * seconds (environment, default 1800: a hung or dead peer), aborts the communicator
+ * (ncclCommAbort) and returns ENCCL; the ctx then needs pgpcv_shard again. */
 int pgpcv_shard(pgpcv_ctx *ctx, int rank, int world, const void *nccl_unique_id);
+
+/* Which libnccl the library bound (it reuses an NCCL already loaded in the process, e.g.
+ * torch's, so one process never holds two): "path (NCCL x.y.z)" into buf[len], or the
+ * reason none could be loaded.  Needs no ctx.  Errors: EINVAL (NULL / len < 1), ENCCL
+ * (no usable libnccl; buf holds the reason). */
+int pgpcv_nccl_library(char *buf, int64_t len);
 
 /* Fill `out` (NCCL_UNIQUE_ID_BYTES bytes) with a fresh ncclUniqueId.  Needs no ctx.
  * Errors: ENCCL (libnccl.so.2 not loadable), EINVAL (NULL). */
@@ -305,8 +327,22 @@ int pgpcv_last_timing(const pgpcv_ctx *ctx, pgpcv_timing *out);
 /* Host-only helper (no GPU needed): LPT assignment of n_items with costs cost[] to
  * `world` owners -- items in descending cost (ties: ascending index), each to the
  * currently least-loaded owner (ties: lowest rank).  owner: int32[n_items] out.
- * This is the rule pgpcv_shard applies to the subsets (cost = k^3 if m > 0 else 0). */
+ * This is the rule every evaluation applies after pgpcv_shard, over the subsets it
+ * factors in ascending subset id (CV: subsets with validation data; with the likelihood:
+ * every subset; predict: subsets with targets; GLS: subsets with training data), cost k^3. */
 int pgpcv_lpt_assign(int64_t n_items, const double *cost, int32_t world, int32_t *owner);
+
+/* Diagnostic (no part of the method's data path): evaluate one of the kernel's elementary
+ * FP64 functions on n host values x -> y (caller-owned host arrays), on the ctx device with
+ * the exact device code the CV kernel inlines, so their accuracy can be tested directly.
+ *   fn = PGPCV_MATH_EXP_NEG: exp(x) for x <= 0 (the covariance exp(-d/range));
+ *        PGPCV_MATH_SQRT:    sqrt(x) for x >= 0 (the distance of squared offsets);
+ *        PGPCV_MATH_RSQRT:   1/sqrt(x) for x > 0 (the Cholesky pivots).
+ * Errors: EINVAL (bad fn, n < 0, NULL), ECUDA, ENOMEM. */
+#define PGPCV_MATH_EXP_NEG 0
+#define PGPCV_MATH_SQRT 1
+#define PGPCV_MATH_RSQRT 2
+int pgpcv_device_math(pgpcv_ctx *ctx, int32_t fn, int64_t n, const double *x, double *y);
 
 #ifdef __cplusplus
 }

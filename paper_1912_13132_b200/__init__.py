@@ -33,9 +33,11 @@ EXPORTED = ("pgpcv_version", "pgpcv_create", "pgpcv_destroy", "pgpcv_last_error"
             "pgpcv_partition_bisect", "pgpcv_partition_bisect_device", "pgpcv_partition_rects",
             "pgpcv_partition_export", "pgpcv_shard", "pgpcv_nccl_get_unique_id",
             "pgpcv_cv_loss", "pgpcv_evaluate", "pgpcv_select", "pgpcv_predict",
-            "pgpcv_partition_export_test", "pgpcv_gls", "pgpcv_last_timing", "pgpcv_lpt_assign")
+            "pgpcv_partition_export_test", "pgpcv_gls", "pgpcv_last_timing", "pgpcv_lpt_assign",
+            "pgpcv_nccl_library", "pgpcv_device_math")
 ROLE_TRAIN, ROLE_VALIDATION, ROLE_TEST = 0, 1, 2
-ABI_VERSION = 4
+ABI_VERSION = 5
+MATH_EXP_NEG, MATH_SQRT, MATH_RSQRT = 0, 1, 2
 
 
 class PgpcvError(RuntimeError):
@@ -70,7 +72,8 @@ class Outputs(ctypes.Structure):
 class Timing(ctypes.Structure):
     _fields_ = [("kernel_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
                 ("flops", ctypes.c_double), ("n_evals", ctypes.c_int64),
-                ("launches", ctypes.c_int32), ("n_slots", ctypes.c_int32)]
+                ("launches", ctypes.c_int32), ("n_slots", ctypes.c_int32),
+                ("n_configs_executed", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -113,6 +116,8 @@ def load_library():
     lib.pgpcv_gls.argtypes = [p, p, i32, Param, p, p, p]
     lib.pgpcv_last_timing.argtypes = [p, ctypes.POINTER(Timing)]
     lib.pgpcv_lpt_assign.argtypes = [i64, p, i32, p]
+    lib.pgpcv_nccl_library.argtypes = [p, i64]
+    lib.pgpcv_device_math.argtypes = [p, i32, i64, p, p]
     for name in EXPORTED:
         if name not in ("pgpcv_destroy", "pgpcv_last_error"):
             getattr(lib, name).restype = ctypes.c_int
@@ -136,6 +141,13 @@ def lpt_assign(cost, world: int) -> np.ndarray:
     if rc:
         raise PgpcvError(rc, "pgpcv_lpt_assign")
     return owner
+
+
+def nccl_library() -> str:
+    """pgpcv_nccl_library: the libnccl the library bound, "path (NCCL x.y.z)" (or why none)."""
+    buf = ctypes.create_string_buffer(4096)
+    load_library().pgpcv_nccl_library(buf, len(buf))
+    return buf.value.decode()
 
 
 def nccl_unique_id() -> bytes:
@@ -402,6 +414,13 @@ class Context:
         self._check(self._lib.pgpcv_partition_export_test(self._h, _ptr(off), _ptr(idx)),
                     "pgpcv_partition_export_test")
         return off, idx
+
+    def device_math(self, fn: int, x) -> np.ndarray:
+        """pgpcv_device_math (diagnostic): the CV kernel's exp_neg / sqrt / rsqrt on x."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        self._check(self._lib.pgpcv_device_math(self._h, int(fn), x.size, _ptr(x), _ptr(y)), "pgpcv_device_math")
+        return y
 
     def last_timing(self) -> dict:
         t = Timing()

@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             if (tid == 0) {
                 const double qnan = __longlong_as_double(0x7ff8000000000000ll);
                 if (a.flags & kCvPredict) a.subset_loss[oi] = qnan;
-                if (a.flags & kCvNll) a.subset_nll[oi] = qnan;
+                if (a.flags & kCvNll) a.logdet[oi] = a.zz[oi] = qnan;
                 a.fail[oi] = 1;
             }
             continue;
@@ -705,7 +705,9 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
         // ---------------- -2 log-likelihood (Eq.2) from the same factor ----------
         // sigma2 Sigma + tau I = sigma2 (Sigma + lambda I) = sigma2 L L^T, so
         //   log det = k log sigma2 + 2 sum log L_ii,  y^T (.)^{-1} y = ||z||^2 / sigma2,
-        // with z = L^{-1} y_T the bordered row k of the factor.
+        // with z = L^{-1} y_T the bordered row k of the factor.  The item depends on zeta
+        // only through (range, lambda); the sigma2 terms are added per configuration by
+        // expand_kernel, so configurations sharing (range, lambda) share this factor.
         if (a.flags & kCvNll) {
             double zz = 0.0;
             for (int cc = tid; cc < k; cc += NT) {
@@ -718,9 +720,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             if (tid == 0) {
                 double q = 0.0;
                 for (int w = 0; w < NWARP; ++w) q += red[w];
-                const double kd = (double)k;
-                a.subset_nll[oi] = kd * log(2.0 * 3.14159265358979323846) + kd * log(sigma2) +
-                                   2.0 * logdet + q / sigma2;
+                a.logdet[oi] = logdet;
+                a.zz[oi] = q;
             }
             __syncthreads();
         }
@@ -884,6 +885,47 @@ __global__ void reduce_kernel(const double *vals, const uint8_t *fail, const int
     if (status) status[c] = (int32_t)st;
 }
 
+// zeta dedup (pgpcv_evaluate): every configuration c takes the results of its unique
+// (range, lambda) u = umap[c]; the likelihood adds the sigma2 terms of Eq.2,
+//   -2 log L = k log 2pi + k log sigma2 + 2 sum log L_ii + ||z||^2 / sigma2.
+// Subsets this rank did not evaluate hold exact zeros (a sum over ranks is then exact).
+__global__ void expand_kernel(int64_t N, int32_t C, int32_t U, const int32_t *umap, const uint8_t *own,
+                              const int64_t *train_off, const double *sigma2, const double *u_loss,
+                              const uint8_t *u_fail, const double *u_logdet, const double *u_zz, double *loss,
+                              uint8_t *fail, double *nll) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * C; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e / C;
+        const int c = (int)(e - s * C);
+        const int64_t ue = s * U + umap[c];
+        if (!own[s]) {
+            loss[e] = 0.0;
+            fail[e] = 0;
+            if (nll) nll[e] = 0.0;
+            continue;
+        }
+        loss[e] = u_loss[ue];
+        fail[e] = u_fail[ue];
+        if (nll) {
+            const double kd = (double)(train_off[s + 1] - train_off[s]);
+            const double s2 = sigma2[c];
+            nll[e] = u_fail[ue] ? __longlong_as_double(0x7ff8000000000000ll)
+                                : kd * log(2.0 * 3.14159265358979323846) + kd * log(s2) + 2.0 * u_logdet[ue] +
+                                      u_zz[ue] / s2;
+        }
+    }
+}
+
+// Diagnostic: the elementary functions exactly as cv_kernel inlines them.
+__global__ void device_math_kernel(int32_t fn, int64_t n, const double *x, double *y) {
+    __shared__ double etab[EXP_TAB];
+    if (threadIdx.x < EXP_TAB) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[i];
+        y[i] = fn == 0 ? exp_neg(v, etab) : (fn == 1 ? sqrt_nb(v) : rsqrt_nb(v));
+    }
+}
+
 // GLS: W = (p+1) p entries per subset; thread w sums entry w over subsets in ascending s
 // (failed subsets poison the sums), then thread 0 solves A beta = b by Gaussian elimination
 // with partial pivoting (largest |pivot|, first on ties).
@@ -983,6 +1025,24 @@ cudaError_t launch_cv_kernel(const CvArgs &a, int grid, cudaStream_t st) {
                                          (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     cv_kernel<<<grid, NT, SMEM_BYTES, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand(int64_t N, int32_t C, int32_t U, const int32_t *umap, const uint8_t *own,
+                          const int64_t *train_off, const double *sigma2, const double *u_loss,
+                          const uint8_t *u_fail, const double *u_logdet, const double *u_zz, double *loss,
+                          uint8_t *fail, double *nll, cudaStream_t st) {
+    if (N * C == 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>((N * C + 255) / 256, 148 * 8);
+    expand_kernel<<<grid, 256, 0, st>>>(N, C, U, umap, own, train_off, sigma2, u_loss, u_fail, u_logdet, u_zz, loss,
+                                        fail, nll);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_device_math(int32_t fn, int64_t n, const double *x, double *y, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    device_math_kernel<<<grid, 256, 0, st>>>(fn, n, x, y);
     return cudaGetLastError();
 }
 

@@ -2,6 +2,9 @@
 // memory and stream ownership, work scheduling (LPT), the NCCL combine step, timing.
 // Every numerical step runs in the kernels of partition.cu and cv_kernel.cu.
 #include <dlfcn.h>
+#include <sched.h>
+#include <time.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -59,21 +62,32 @@ struct DevBuf {
 struct NcclApi {
     bool ok = false;
     std::string why;
+    std::string where;  // the bound library: path (dladdr) and version, or why none
     ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
                               ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*getVersion)(int *) = nullptr;
     const char *(*getErrorString)(ncclResult_t) = nullptr;
 };
+
+// Any already-loaded object that exports ncclGetUniqueId (torch's libtorch_cuda links its
+// bundled NCCL statically or as libnccl.so.2): reuse it so one process never holds two NCCLs.
+void *nccl_already_loaded() {
+    if (void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD)) return h;
+    if (dlsym(RTLD_DEFAULT, "ncclGetUniqueId")) return RTLD_DEFAULT;
+    return nullptr;
+}
 
 NcclApi &nccl() {
     static NcclApi api;
     static bool tried = false;
     if (tried) return api;
     tried = true;
-    // Prefer an already-loaded libnccl (torch's bundled copy) so one process never holds two.
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    void *h = nccl_already_loaded();
     if (!h) {
         const char *env = getenv("PGPCV_NCCL_LIB");
         if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
@@ -81,17 +95,39 @@ NcclApi &nccl() {
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
         api.why = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+        api.where = api.why;
         return api;
     }
     api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
     api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
     api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.commAbort = (decltype(api.commAbort))dlsym(h, "ncclCommAbort");
+    api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    api.getVersion = (decltype(api.getVersion))dlsym(h, "ncclGetVersion");
     api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
-    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy &&
-             api.getErrorString;
-    if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.commAbort &&
+             api.commGetAsyncError && api.getVersion && api.getErrorString;
+    if (!api.ok) {
+        api.why = "libnccl.so.2 lacks a required symbol";
+        api.where = api.why;
+        return api;
+    }
+    Dl_info info{};
+    const char *path = dladdr((void *)api.getUniqueId, &info) && info.dli_fname ? info.dli_fname : "?";
+    int v = 0;
+    api.getVersion(&v);
+    char buf[1024];
+    snprintf(buf, sizeof buf, "%s (NCCL %d.%d.%d)", path, v / 10000, (v / 100) % 100, v % 100);
+    api.where = buf;
+    if (getenv("PGPCV_VERBOSE")) fprintf(stderr, "libpgpcv: NCCL bound from %s\n", buf);
     return api;
+}
+
+double now_s() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
 }
 
 std::string g_create_error;
@@ -100,6 +136,10 @@ std::string g_create_error;
 __global__ void status_encode(int32_t *st, int32_t C, int32_t sentinel) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c < C && st[c] == sentinel) st[c] = (sentinel == -1) ? 0x7fffffff : -1;
+}
+cudaError_t launch_status_encode(int32_t *st, int32_t C, int32_t sentinel, cudaStream_t stream) {
+    status_encode<<<(C + 127) / 128, 128, 0, stream>>>(st, C, sentinel);
+    return cudaGetLastError();
 }
 
 // R4: e_i = a + i*w (separate multiply and add), e_K = b; bounds e_i - delta, e_{i+1} + delta.
@@ -134,6 +174,7 @@ struct pgpcv_ctx {
     cudaMemPool_t pool = nullptr;  // partition scratch; keeps its memory between calls
     std::string err;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_sync = nullptr;  // completion polling of collectives (no timing)
 
     // partition state
     bool has_partition = false;
@@ -158,6 +199,9 @@ struct pgpcv_ctx {
     // sharding
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    bool comm_aborted = false;  // a collective failed or timed out: shard again
+    double nccl_timeout_s = 1800.0;
+    DevBuf<int32_t> errflag;    // rank-local error flag for the lockstep all-reduce
     bool cv_done = false;
     std::vector<uint8_t> owned;
 
@@ -168,6 +212,12 @@ struct pgpcv_ctx {
     DevBuf<unsigned long long> counter;
     DevBuf<double> subset_loss, subset_nll, sums;  // sums: [loss C | nll C]
     DevBuf<uint8_t> fail;
+    // per-unique-(range, lambda) kernel outputs (zeta dedup), expanded to the C configs
+    DevBuf<double> u_loss, u_logdet, u_zz;
+    DevBuf<uint8_t> u_fail;
+    DevBuf<int32_t> u_map;
+    DevBuf<double> u_sigma2;
+    DevBuf<uint8_t> own_mask;  // [N] subsets this rank evaluated in the last call
     DevBuf<int32_t> status;                        // [loss C | nll C]
     // pgpcv_predict
     DevBuf<double> p_sub, p_yhat, p_sum;
@@ -210,18 +260,32 @@ struct pgpcv_ctx {
 
 namespace {
 
-void assign_owned(pgpcv_ctx *ctx) {
+// Ownership of the subsets a call evaluates (`work[s]` != 0): LPT on k_s^3 over exactly
+// those subsets (the rule documented at pgpcv_lpt_assign), so every mode balances the
+// factorizations it actually runs (the likelihood and GLS factor subsets without
+// validation data too).  A pure function of the partition and the call's mode, hence
+// identical on every rank.  World 1 owns everything.
+void assign_owned(pgpcv_ctx *ctx, const std::vector<uint8_t> &work) {
     ctx->owned.assign(ctx->N, 1);
     if (ctx->world <= 1) return;
-    std::vector<double> cost(ctx->N);
+    std::vector<int64_t> ids;
+    std::vector<double> cost;
     for (int64_t s = 0; s < ctx->N; ++s) {
+        if (!work[s]) continue;
         const double k = (double)(ctx->h_train_off[s + 1] - ctx->h_train_off[s]);
-        const double m = (double)(ctx->h_val_off[s + 1] - ctx->h_val_off[s]);
-        cost[s] = m > 0 ? k * k * k : 0.0;  // the rule documented in pgpcv.h
+        ids.push_back(s);
+        cost.push_back(k * k * k);
     }
-    std::vector<int32_t> owner(ctx->N);
-    pgpcv_lpt_assign(ctx->N, cost.data(), ctx->world, owner.data());
-    for (int64_t s = 0; s < ctx->N; ++s) ctx->owned[s] = owner[s] == ctx->rank;
+    std::vector<int32_t> owner(ids.size());
+    pgpcv_lpt_assign((int64_t)ids.size(), cost.data(), ctx->world, owner.data());
+    for (int64_t s = 0; s < ctx->N; ++s) ctx->owned[s] = 0;
+    for (size_t i = 0; i < ids.size(); ++i) ctx->owned[ids[i]] = owner[i] == ctx->rank;
+}
+
+void reset_shard(pgpcv_ctx *ctx) {
+    ctx->rank = 0;
+    ctx->world = 1;
+    ctx->comm = nullptr;
 }
 
 // How the subsets are formed: equal tiles (R1) or the recursive bisection (row f2).
@@ -398,7 +462,7 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     ctx->has_partition = true;
     ctx->cv_done = false;
     ctx->sel_C = 0;
-    assign_owned(ctx);
+    ctx->owned.assign(N, 1);  // each evaluation assigns its own work (assign_owned)
     if (info_out) *info_out = info;
     return PGPCV_OK;
 }
@@ -462,6 +526,7 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     }
     if (const char *env = getenv("PGPCV_SCHED")) ctx->sched = atoi(env);
     for (auto &ev : ctx->ev) cudaEventCreate(&ev);
+    cudaEventCreateWithFlags(&ctx->ev_sync, cudaEventDisableTiming);
     if ((e = cv_kernel_occupancy(&ctx->blocks_per_sm)) != cudaSuccess || ctx->blocks_per_sm < 1) {
         g_create_error = std::string("cv kernel cannot be resident: ") + cudaGetErrorString(e);
         pgpcv_destroy(ctx);
@@ -478,6 +543,7 @@ void pgpcv_destroy(pgpcv_ctx *ctx) {
     if (ctx->comm && nccl().ok) nccl().commDestroy(ctx->comm);
     for (auto &ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
+    if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
@@ -634,31 +700,42 @@ int pgpcv_shard(pgpcv_ctx *ctx, int rank, int world, const void *nccl_unique_id)
     if (world < 1 || rank < 0 || rank >= world)
         return ctx->fail_with(PGPCV_EINVAL, "need 0 <= rank < world");
     if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "pgpcv_shard needs a partition");
-    if (ctx->cv_done)
+    if (ctx->cv_done && !ctx->comm_aborted)
         return ctx->fail_with(PGPCV_ESTATE, "pgpcv_shard after pgpcv_cv_loss on this partition");
+    // Validate every prerequisite before touching the ctx's sharding state: a failed call
+    // leaves the ctx at rank 0 of world 1 (it then owns every subset and runs no collective).
+    NcclApi *api = nullptr;
+    if (world > 1) {
+        if (!nccl_unique_id) return ctx->fail_with(PGPCV_EINVAL, "world > 1 needs an ncclUniqueId");
+        api = &nccl();
+        if (!api->ok) return ctx->fail_with(PGPCV_ENCCL, "%s", api->why.c_str());
+    }
     cudaSetDevice(ctx->device);
     if (ctx->comm) {
         nccl().commDestroy(ctx->comm);
         ctx->comm = nullptr;
     }
-    ctx->rank = rank;
-    ctx->world = world;
+    reset_shard(ctx);
+    ctx->comm_aborted = false;
     if (world > 1) {
-        if (!nccl_unique_id) return ctx->fail_with(PGPCV_EINVAL, "world > 1 needs an ncclUniqueId");
-        NcclApi &api = nccl();
-        if (!api.ok) return ctx->fail_with(PGPCV_ENCCL, "%s", api.why.c_str());
         ncclUniqueId id;
         memcpy(&id, nccl_unique_id, sizeof id);
-        ncclResult_t r = api.commInitRank(&ctx->comm, world, id, rank);
-        if (r != ncclSuccess) {
-            ctx->comm = nullptr;
-            ctx->world = 1;
-            ctx->rank = 0;
-            return ctx->fail_with(PGPCV_ENCCL, "ncclCommInitRank: %s", api.getErrorString(r));
-        }
+        ncclComm_t comm = nullptr;
+        ncclResult_t r = api->commInitRank(&comm, world, id, rank);
+        if (r != ncclSuccess) return ctx->fail_with(PGPCV_ENCCL, "ncclCommInitRank: %s", api->getErrorString(r));
+        ctx->comm = comm;
+        ctx->rank = rank;
+        ctx->world = world;
     }
-    assign_owned(ctx);
+    if (const char *env = getenv("PGPCV_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = atof(env);
     return PGPCV_OK;
+}
+
+int pgpcv_nccl_library(char *buf, int64_t len) {
+    if (!buf || len < 1) return PGPCV_EINVAL;
+    NcclApi &api = nccl();
+    snprintf(buf, (size_t)len, "%s", api.where.c_str());
+    return api.ok ? PGPCV_OK : PGPCV_ENCCL;
 }
 
 }  // extern "C"
@@ -687,7 +764,7 @@ struct CvLaunch {
     int32_t out_C = 1;
     const int64_t *tgt_off = nullptr;
     const double *gx = nullptr, *gy = nullptr, *gv = nullptr;
-    double *subset_loss = nullptr, *subset_nll = nullptr, *yhat = nullptr;
+    double *subset_loss = nullptr, *logdet = nullptr, *zz = nullptr, *yhat = nullptr;
     uint8_t *fail = nullptr;
     int launches = 0;  // kernel launches run_cv made
     int32_t p = 0;  // GLS covariates (bordered rows below y)
@@ -761,7 +838,8 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.out_C = L.out_C;
         a.flags = L.flags;
         a.subset_loss = L.subset_loss;
-        a.subset_nll = L.subset_nll;
+        a.logdet = L.logdet;
+        a.zz = L.zz;
         a.yhat = L.yhat;
         a.fail = L.fail;
         a.p = L.p;
@@ -815,7 +893,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     return PGPCV_OK;
 }
 
-void record_timing(pgpcv_ctx *ctx, const CvLaunch &L, int launches) {
+void record_timing(pgpcv_ctx *ctx, const CvLaunch &L, int launches, int32_t configs_executed) {
     float kms = 0, tms = 0;
     cudaEventElapsedTime(&kms, ctx->ev[1], ctx->ev[2]);
     cudaEventElapsedTime(&tms, ctx->ev[0], ctx->ev[3]);
@@ -825,17 +903,113 @@ void record_timing(pgpcv_ctx *ctx, const CvLaunch &L, int launches) {
     ctx->timing.n_evals = (int64_t)L.items.size();
     ctx->timing.launches = launches;
     ctx->timing.n_slots = L.slots;
+    ctx->timing.n_configs_executed = configs_executed;
     ctx->has_timing = true;
 }
 
-int nccl_sum(pgpcv_ctx *ctx, void *buf, size_t count, ncclDataType_t t) {
+int nccl_sum(pgpcv_ctx *ctx, void *buf, size_t count, ncclDataType_t t, ncclRedOp_t op = ncclSum) {
     NcclApi &api = nccl();
-    ncclResult_t r = api.allReduce(buf, buf, count, t, ncclSum, ctx->comm, ctx->stream);
+    ncclResult_t r = api.allReduce(buf, buf, count, t, op, ctx->comm, ctx->stream);
     if (r != ncclSuccess) return ctx->fail_with(PGPCV_ENCCL, "ncclAllReduce: %s", api.getErrorString(r));
     return PGPCV_OK;
 }
 
+// Wait for the work enqueued on the ctx stream (collectives included) while polling the
+// communicator for asynchronous errors.  An NCCL error, or no completion within
+// nccl_timeout_s (a hung or dead peer), aborts the communicator: the call returns ENCCL and
+// the ctx needs pgpcv_shard again before another multi-rank evaluation.
+int wait_collective(pgpcv_ctx *ctx, const char *what) {
+    NcclApi &api = nccl();
+    CK(cudaEventRecord(ctx->ev_sync, ctx->stream), "event");
+    const double t0 = now_s();
+    for (long spins = 0;; ++spins) {
+        const cudaError_t q = cudaEventQuery(ctx->ev_sync);
+        if (q == cudaSuccess) return PGPCV_OK;
+        if (q != cudaErrorNotReady) return ctx->cuda_fail(q, what);
+        ncclResult_t ar = ncclSuccess;
+        api.commGetAsyncError(ctx->comm, &ar);
+        const bool bad = ar != ncclSuccess && ar != ncclInProgress;
+        const double waited = now_s() - t0;
+        if (bad || waited > ctx->nccl_timeout_s) {
+            api.commAbort(ctx->comm);
+            ctx->comm = nullptr;
+            ctx->comm_aborted = true;
+            if (bad)
+                return ctx->fail_with(PGPCV_ENCCL, "%s: NCCL error %s (communicator aborted; call pgpcv_shard again)",
+                                      what, api.getErrorString(ar));
+            return ctx->fail_with(PGPCV_ENCCL, "%s: no completion after %.0f s (a peer hung or died; communicator "
+                                  "aborted; call pgpcv_shard again)", what, waited);
+        }
+        if (spins < 2000)
+            sched_yield();
+        else
+            usleep(100);
+    }
+}
+
+// End of a call: world 1 synchronises the stream; world > 1 polls (wait_collective).
+int finish(pgpcv_ctx *ctx, const char *what) {
+    if (ctx->world > 1) {
+        int rc = wait_collective(ctx, what);
+        if (rc) return rc;
+    } else {
+        CK(cudaStreamSynchronize(ctx->stream), what);
+    }
+    CK(cudaGetLastError(), what);
+    return PGPCV_OK;
+}
+
+// Lockstep of the ranks (world > 1): every rank arrives here after its rank-local work
+// with its outcome rc (argument checks that depend on the whole partition ran before any
+// rank-local work, identically on every rank).  One MAX all-reduce of the error flags
+// decides for all ranks together whether the data collectives run, so no rank enqueues a
+// collective that a failed peer will never join.  Returns rc, or ENCCL when a peer failed.
+int join_ranks(pgpcv_ctx *ctx, int rc) {
+    if (ctx->world <= 1) return rc;
+    if (const char *f = getenv("PGPCV_TEST_FAIL_RANK"))  // fault injection for the lockstep test
+        if (rc == PGPCV_OK && atoi(f) == ctx->rank)
+            rc = ctx->fail_with(PGPCV_ENOMEM, "injected rank-local failure (PGPCV_TEST_FAIL_RANK)");
+    if (rc == PGPCV_OK) {  // the local work must be complete, asynchronous errors included
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) rc = ctx->cuda_fail(e, "rank-local evaluation");
+    }
+    const std::string local_err = ctx->err;
+    int32_t flag = rc ? 1 : 0;
+    CK(ctx->errflag.ensure(1), "alloc");
+    CK(cudaMemcpyAsync(ctx->errflag.p, &flag, sizeof flag, cudaMemcpyHostToDevice, ctx->stream), "copy flag");
+    int r2 = nccl_sum(ctx, ctx->errflag.p, 1, ncclInt32, ncclMax);
+    if (!r2) {
+        CK(cudaMemcpyAsync(&flag, ctx->errflag.p, sizeof flag, cudaMemcpyDeviceToHost, ctx->stream), "copy flag");
+        r2 = wait_collective(ctx, "error-flag all-reduce");
+    }
+    if (rc) {
+        ctx->err = local_err;
+        return rc;
+    }
+    if (r2) return r2;
+    if (flag) return ctx->fail_with(PGPCV_ENCCL, "a peer rank failed its local evaluation");
+    return PGPCV_OK;
+}
+
+// Checks that must give the same answer on every rank, before any rank-local work.
+int check_common(pgpcv_ctx *ctx) {
+    if (ctx->info.max_k > cv_kernel_max_k())
+        return ctx->fail_with(PGPCV_EINVAL, "a subset has %lld training points (max %d)",
+                              (long long)ctx->info.max_k, cv_kernel_max_k());
+    if (ctx->world > 1 && !ctx->comm)
+        return ctx->fail_with(PGPCV_ENCCL, "the communicator was aborted by an earlier failure; call pgpcv_shard "
+                                           "again");
+    return PGPCV_OK;
+}
+
 int first_fail(int32_t a, int32_t b) { return a < 0 ? b : (b < 0 ? a : std::min(a, b)); }
+
+uint64_t dbits(double v) {
+    uint64_t u;
+    memcpy(&u, &v, sizeof u);
+    return u;
+}
 
 }  // namespace
 
@@ -851,53 +1025,106 @@ int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, 
     const bool want_nll = out->nll || out->subset_nll;
     if (!want_cv && !want_nll) return ctx->fail_with(PGPCV_EINVAL, "no output requested");
     if (want_cv && ctx->info.sum_m == 0) return ctx->fail_with(PGPCV_EEMPTY, "no subset has validation data");
+    if ((rc = check_common(ctx))) return rc;
     cudaSetDevice(ctx->device);
     cudaStream_t st = ctx->stream;
     const int64_t N = ctx->N;
     const int32_t C = n_params;
     ctx->sel_C = 0;
 
+    // zeta dedup (the prediction depends on zeta only through (range, lambda), lambda
+    // = nugget / sigma2): configs whose (range, lambda) are bit-identical share one
+    // factorization per subset.  lambda is the same IEEE division the kernel performs, so
+    // the shared results are exactly those each config would compute.  Nothing is cached
+    // across calls.
+    std::vector<int32_t> umap(C);
+    std::vector<pgpcv_param> uparams;
+    std::vector<double> sig2(C);
+    {
+        std::vector<std::pair<uint64_t, uint64_t>> keys;
+        for (int32_t c = 0; c < C; ++c) {
+            const volatile double lam = params[c].nugget / params[c].sigma2;
+            const std::pair<uint64_t, uint64_t> key(dbits(params[c].range), dbits(lam));
+            int32_t u = (int32_t)(std::find(keys.begin(), keys.end(), key) - keys.begin());
+            if (u == (int32_t)keys.size()) {
+                keys.push_back(key);
+                uparams.push_back(params[c]);
+            }
+            umap[c] = u;
+            sig2[c] = params[c].sigma2;
+        }
+    }
+    const int32_t U = (int32_t)uparams.size();
+
     CvLaunch L;
     L.flags = (want_cv ? kCvPredict : 0) | (want_nll ? kCvNll : 0);
-    L.params = params;
-    L.C = C;
-    L.out_C = C;
+    L.params = uparams.data();
+    L.C = U;
+    L.out_C = U;
     L.tgt_off = ctx->val_off.p;
     L.gx = ctx->vx.p;
     L.gy = ctx->vy.p;
     L.gv = ctx->vv.p;
-    // work items: owned subsets with validation data (all owned subsets when the likelihood
-    // is requested: it needs no targets), every config
+    // subsets this call factors: those with validation data, every subset when the
+    // likelihood is requested (it needs no targets); this rank's share by LPT on k^3
+    std::vector<uint8_t> work(N), own(N);
+    for (int64_t s = 0; s < N; ++s) work[s] = (ctx->h_val_off[s + 1] > ctx->h_val_off[s]) || want_nll;
+    assign_owned(ctx, work);
     for (int64_t s = 0; s < N; ++s) {
+        own[s] = work[s] && ctx->owned[s];
+        if (!own[s]) continue;
         const int64_t k = ctx->h_train_off[s + 1] - ctx->h_train_off[s];
         const int64_t m = ctx->h_val_off[s + 1] - ctx->h_val_off[s];
-        if (!ctx->owned[s] || (m == 0 && !want_nll)) continue;
-        for (int32_t c = 0; c < C; ++c) L.items.push_back(make_int2((int)s, c));
-        // the Cholesky and forward solve count for every item; the backward
-        // solve, prediction and residuals only where validation data are predicted.
+        for (int32_t u = 0; u < U; ++u) L.items.push_back(make_int2((int)s, u));
+        // the Cholesky and forward solve count for every executed item; the
+        // backward solve, prediction and residuals only where validation data are predicted.
         const double kd = (double)k, md = (double)m;
         double f = kd * kd * kd / 3.0 + kd * kd / 2.0 + kd / 6.0 + kd * kd;
         if (want_cv && m > 0) f += kd * kd + 2.0 * md * kd + 3.0 * md;
-        L.flops += C * f;
+        L.flops += U * f;
     }
-    CK(ctx->subset_loss.ensure((size_t)N * C), "alloc subset_loss");
-    CK(ctx->subset_nll.ensure((size_t)N * C), "alloc subset_nll");
-    CK(ctx->fail.ensure((size_t)N * C), "alloc fail");
-    CK(ctx->sums.ensure(2 * (size_t)C), "alloc sums");
-    CK(ctx->status.ensure(2 * (size_t)C), "alloc status");
-    L.subset_loss = ctx->subset_loss.p;
-    L.subset_nll = ctx->subset_nll.p;
-    L.fail = ctx->fail.p;
-
-    CK(cudaEventRecord(ctx->ev[0], st), "event");
-    CK(cudaMemsetAsync(ctx->subset_loss.p, 0, sizeof(double) * N * C, st), "memset");
-    CK(cudaMemsetAsync(ctx->subset_nll.p, 0, sizeof(double) * N * C, st), "memset");
-    CK(cudaMemsetAsync(ctx->fail.p, 0, (size_t)N * C, st), "memset");
-    if ((rc = run_cv(ctx, L))) return rc;
-    int launches = L.launches;
-
     const bool multi = ctx->world > 1;
     const bool gather = multi && (out->subset_loss || out->subset_nll);
+    int launches = 0;
+
+    // ---- rank-local phase: factor this rank's (subset, unique config) items ----
+    auto local = [&]() -> int {
+        CK(ctx->subset_loss.ensure((size_t)N * C), "alloc subset_loss");
+        CK(ctx->subset_nll.ensure((size_t)N * C), "alloc subset_nll");
+        CK(ctx->fail.ensure((size_t)N * C), "alloc fail");
+        CK(ctx->u_loss.ensure((size_t)N * U), "alloc");
+        CK(ctx->u_fail.ensure((size_t)N * U), "alloc");
+        CK(ctx->u_logdet.ensure(want_nll ? (size_t)N * U : 1), "alloc");
+        CK(ctx->u_zz.ensure(want_nll ? (size_t)N * U : 1), "alloc");
+        CK(ctx->u_map.ensure(C), "alloc");
+        CK(ctx->u_sigma2.ensure(C), "alloc");
+        CK(ctx->own_mask.ensure(N), "alloc");
+        CK(ctx->sums.ensure(2 * (size_t)C), "alloc sums");
+        CK(ctx->status.ensure(2 * (size_t)C), "alloc status");
+        L.subset_loss = ctx->u_loss.p;
+        L.logdet = want_nll ? ctx->u_logdet.p : nullptr;
+        L.zz = want_nll ? ctx->u_zz.p : nullptr;
+        L.fail = ctx->u_fail.p;
+        CK(cudaEventRecord(ctx->ev[0], st), "event");
+        CK(cudaMemcpyAsync(ctx->u_map.p, umap.data(), sizeof(int32_t) * C, cudaMemcpyHostToDevice, st), "copy");
+        CK(cudaMemcpyAsync(ctx->u_sigma2.p, sig2.data(), sizeof(double) * C, cudaMemcpyHostToDevice, st), "copy");
+        CK(cudaMemcpyAsync(ctx->own_mask.p, own.data(), (size_t)N, cudaMemcpyHostToDevice, st), "copy");
+        CK(cudaMemsetAsync(ctx->u_loss.p, 0, sizeof(double) * N * U, st), "memset");
+        CK(cudaMemsetAsync(ctx->u_fail.p, 0, (size_t)N * U, st), "memset");
+        int r = run_cv(ctx, L);
+        if (r) return r;
+        launches = L.launches;
+        // unique configs -> configs (and -2 log L per sigma2); zeros where this rank did
+        // not evaluate, so a sum over ranks is exact
+        CK(launch_expand(N, C, U, ctx->u_map.p, ctx->own_mask.p, ctx->train_off.p, ctx->u_sigma2.p, ctx->u_loss.p,
+                         ctx->u_fail.p, L.logdet, L.zz, ctx->subset_loss.p, ctx->fail.p,
+                         want_nll ? ctx->subset_nll.p : nullptr, st), "expand");
+        ++launches;
+        return PGPCV_OK;
+    };
+    if ((rc = join_ranks(ctx, local()))) return rc;
+
+    // ---- combine (Alg.1 line 9) ----
     if (gather) {
         // each (s, c) entry has exactly one owner (others hold 0): the sums are exact, and
         // the global reductions below then run on identical arrays on every rank.
@@ -923,12 +1150,10 @@ int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, 
         if (!want_cv) CK(cudaMemsetAsync(d_st_loss, 0xff, sizeof(int32_t) * C, st), "memset");
         if (!want_nll) CK(cudaMemsetAsync(d_st_nll, 0xff, sizeof(int32_t) * C, st), "memset");
         if ((rc = nccl_sum(ctx, ctx->sums.p, 2 * (size_t)C, ncclFloat64))) return rc;
-        status_encode<<<(2 * C + 127) / 128, 128, 0, st>>>(ctx->status.p, 2 * C, -1);
-        NcclApi &api = nccl();
-        ncclResult_t r = api.allReduce(ctx->status.p, ctx->status.p, 2 * (size_t)C, ncclInt32, ncclMin, ctx->comm, st);
-        status_encode<<<(2 * C + 127) / 128, 128, 0, st>>>(ctx->status.p, 2 * C, 0x7fffffff);
+        CK(launch_status_encode(ctx->status.p, 2 * C, -1, st), "status");
+        if ((rc = nccl_sum(ctx, ctx->status.p, 2 * (size_t)C, ncclInt32, ncclMin))) return rc;
+        CK(launch_status_encode(ctx->status.p, 2 * C, 0x7fffffff, st), "status");
         launches += 2;
-        if (r != ncclSuccess) return ctx->fail_with(PGPCV_ENCCL, "ncclAllReduce: %s", api.getErrorString(r));
     }
     std::vector<double> hsums(2 * (size_t)C);
     std::vector<int32_t> hstatus(2 * (size_t)C, -1);
@@ -942,10 +1167,9 @@ int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, 
         CK(cudaMemcpyAsync(out->subset_nll, ctx->subset_nll.p, sizeof(double) * N * C, cudaMemcpyDeviceToHost, st),
            "copy subset_nll");
     CK(cudaEventRecord(ctx->ev[3], st), "event");
-    CK(cudaStreamSynchronize(st), "evaluate");
-    CK(cudaGetLastError(), "evaluate");
+    if ((rc = finish(ctx, "evaluate"))) return rc;
     ctx->cv_done = true;
-    record_timing(ctx, L, launches);
+    record_timing(ctx, L, launches, U);
     if (want_cv && (!multi || gather)) ctx->sel_C = C;  // every subset's loss is on this device
 
     bool any_fail = false;
@@ -1014,6 +1238,7 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
             if (subset_config[s] < 0 || subset_config[s] >= n_params)
                 return ctx->fail_with(PGPCV_EINVAL, "subset_config[%lld] = %d not in [0, %d)", (long long)s,
                                       subset_config[s], n_params);
+    if ((rc = check_common(ctx))) return rc;
     cudaSetDevice(ctx->device);
     cudaStream_t st = ctx->stream;
     const bool test = target_role == PGPCV_ROLE_TEST;
@@ -1029,6 +1254,9 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
     L.gx = test ? ctx->gx.p : ctx->vx.p;
     L.gy = test ? ctx->gy.p : ctx->vy.p;
     L.gv = test ? ctx->gv.p : ctx->vv.p;
+    std::vector<uint8_t> work(N);
+    for (int64_t s = 0; s < N; ++s) work[s] = hoff[s + 1] > hoff[s];
+    assign_owned(ctx, work);
     for (int64_t s = 0; s < N; ++s) {
         const int64_t k = ctx->h_train_off[s + 1] - ctx->h_train_off[s];
         const int64_t m = hoff[s + 1] - hoff[s];
@@ -1037,21 +1265,25 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
         const double kd = (double)k, md = (double)m;
         L.flops += kd * kd * kd / 3.0 + kd * kd / 2.0 + kd / 6.0 + 2.0 * kd * kd + 2.0 * md * kd + 3.0 * md;
     }
-    CK(ctx->p_sub.ensure(N), "alloc");
-    CK(ctx->p_fail.ensure(N), "alloc");
-    CK(ctx->p_yhat.ensure(std::max<int64_t>(n_tgt, 1)), "alloc");
-    CK(ctx->p_sum.ensure(1), "alloc");
-    CK(ctx->p_status.ensure(1), "alloc");
-    L.subset_loss = ctx->p_sub.p;
-    L.fail = ctx->p_fail.p;
-    L.yhat = yhat ? ctx->p_yhat.p : nullptr;
-
-    CK(cudaEventRecord(ctx->ev[0], st), "event");
-    CK(cudaMemsetAsync(ctx->p_sub.p, 0, sizeof(double) * N, st), "memset");
-    CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
-    if (yhat) CK(cudaMemsetAsync(ctx->p_yhat.p, 0, sizeof(double) * std::max<int64_t>(n_tgt, 1), st), "memset");
-    if ((rc = run_cv(ctx, L))) return rc;
-    int launches = L.launches;
+    int launches = 0;
+    auto local = [&]() -> int {
+        CK(ctx->p_sub.ensure(N), "alloc");
+        CK(ctx->p_fail.ensure(N), "alloc");
+        CK(ctx->p_yhat.ensure(std::max<int64_t>(n_tgt, 1)), "alloc");
+        CK(ctx->p_sum.ensure(1), "alloc");
+        CK(ctx->p_status.ensure(1), "alloc");
+        L.subset_loss = ctx->p_sub.p;
+        L.fail = ctx->p_fail.p;
+        L.yhat = yhat ? ctx->p_yhat.p : nullptr;
+        CK(cudaEventRecord(ctx->ev[0], st), "event");
+        CK(cudaMemsetAsync(ctx->p_sub.p, 0, sizeof(double) * N, st), "memset");
+        CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
+        if (yhat) CK(cudaMemsetAsync(ctx->p_yhat.p, 0, sizeof(double) * std::max<int64_t>(n_tgt, 1), st), "memset");
+        int r = run_cv(ctx, L);
+        launches = L.launches;
+        return r;
+    };
+    if ((rc = join_ranks(ctx, local()))) return rc;
     if (ctx->world > 1) {  // exclusive owners: exact sums
         if ((rc = nccl_sum(ctx, ctx->p_sub.p, (size_t)N, ncclFloat64))) return rc;
         if ((rc = nccl_sum(ctx, ctx->p_fail.p, (size_t)N, ncclUint8))) return rc;
@@ -1067,10 +1299,9 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
     if (yhat && n_tgt)
         CK(cudaMemcpyAsync(yhat, ctx->p_yhat.p, sizeof(double) * n_tgt, cudaMemcpyDeviceToHost, st), "copy");
     CK(cudaEventRecord(ctx->ev[3], st), "event");
-    CK(cudaStreamSynchronize(st), "predict");
-    CK(cudaGetLastError(), "predict");
+    if ((rc = finish(ctx, "predict"))) return rc;
     ctx->cv_done = true;
-    record_timing(ctx, L, launches);
+    record_timing(ctx, L, launches, n_params);
     if (sspe) *sspe = total;
     if (status >= 0) return ctx->fail_with(PGPCV_ENUMERIC, "subset %d was not positive definite", status);
     return PGPCV_OK;
@@ -1084,17 +1315,11 @@ int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, dou
     if (!X || !beta) return ctx->fail_with(PGPCV_EINVAL, "NULL X or beta");
     int rc = check_params(ctx, &param, 1);
     if (rc) return rc;
+    if ((rc = check_common(ctx))) return rc;
     cudaSetDevice(ctx->device);
     cudaStream_t st = ctx->stream;
     const int64_t N = ctx->N, n = ctx->n, sum_k = ctx->info.sum_k;
     const int W = (p + 1) * p;
-    CK(ctx->g_X.ensure((size_t)n * p), "alloc");
-    CK(ctx->g_tX.ensure((size_t)sum_k * p), "alloc");
-    CK(ctx->g_part.ensure((size_t)N * W), "alloc");
-    CK(ctx->g_sums.ensure(W), "alloc");
-    CK(ctx->g_beta.ensure(p), "alloc");
-    CK(ctx->p_fail.ensure(N), "alloc");
-    CK(ctx->p_status.ensure(1), "alloc");
     CvLaunch L;
     L.flags = kCvGls;
     L.params = &param;
@@ -1104,10 +1329,10 @@ int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, dou
     L.gx = ctx->vx.p;
     L.gy = ctx->vy.p;
     L.gv = ctx->vv.p;
-    L.fail = ctx->p_fail.p;
     L.p = p;
-    L.tX = ctx->g_tX.p;
-    L.gls_out = ctx->g_part.p;
+    std::vector<uint8_t> work(N);
+    for (int64_t s = 0; s < N; ++s) work[s] = ctx->h_train_off[s + 1] > ctx->h_train_off[s];
+    assign_owned(ctx, work);
     for (int64_t s = 0; s < N; ++s) {
         const int64_t k = ctx->h_train_off[s + 1] - ctx->h_train_off[s];
         if (!ctx->owned[s] || k == 0) continue;
@@ -1116,13 +1341,28 @@ int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, dou
         // Cholesky + (p+1) forward (bordered) and backward solves + core-row sums
         L.flops += kd * kd * kd / 3.0 + kd * kd / 2.0 + kd / 6.0 + (p + 1) * (2.0 * kd * kd + 2.0 * kd * p);
     }
-    CK(cudaEventRecord(ctx->ev[0], st), "event");
-    CK(cudaMemcpyAsync(ctx->g_X.p, X, sizeof(double) * n * p, cudaMemcpyHostToDevice, st), "copy X");
-    CK(launch_gather_rows(sum_k, ctx->train_idx.p, ctx->g_X.p, p, ctx->g_tX.p, st), "gather X");
-    CK(cudaMemsetAsync(ctx->g_part.p, 0, sizeof(double) * N * W, st), "memset");
-    CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
-    if ((rc = run_cv(ctx, L))) return rc;
-    int launches = 1 + L.launches;
+    int launches = 0;
+    auto local = [&]() -> int {
+        CK(ctx->g_X.ensure((size_t)n * p), "alloc");
+        CK(ctx->g_tX.ensure((size_t)sum_k * p), "alloc");
+        CK(ctx->g_part.ensure((size_t)N * W), "alloc");
+        CK(ctx->g_sums.ensure(W), "alloc");
+        CK(ctx->g_beta.ensure(p), "alloc");
+        CK(ctx->p_fail.ensure(N), "alloc");
+        CK(ctx->p_status.ensure(1), "alloc");
+        L.fail = ctx->p_fail.p;
+        L.tX = ctx->g_tX.p;
+        L.gls_out = ctx->g_part.p;
+        CK(cudaEventRecord(ctx->ev[0], st), "event");
+        CK(cudaMemcpyAsync(ctx->g_X.p, X, sizeof(double) * n * p, cudaMemcpyHostToDevice, st), "copy X");
+        CK(launch_gather_rows(sum_k, ctx->train_idx.p, ctx->g_X.p, p, ctx->g_tX.p, st), "gather X");
+        CK(cudaMemsetAsync(ctx->g_part.p, 0, sizeof(double) * N * W, st), "memset");
+        CK(cudaMemsetAsync(ctx->p_fail.p, 0, (size_t)N, st), "memset");
+        int r = run_cv(ctx, L);
+        launches = 1 + L.launches;
+        return r;
+    };
+    if ((rc = join_ranks(ctx, local()))) return rc;
     if (ctx->world > 1) {  // exclusive owners: exact sums
         if ((rc = nccl_sum(ctx, ctx->g_part.p, (size_t)N * W, ncclFloat64))) return rc;
         if ((rc = nccl_sum(ctx, ctx->p_fail.p, (size_t)N, ncclUint8))) return rc;
@@ -1136,10 +1376,9 @@ int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, dou
     CK(cudaMemcpyAsync(sums.data(), ctx->g_sums.p, sizeof(double) * W, cudaMemcpyDeviceToHost, st), "copy");
     CK(cudaMemcpyAsync(&status, ctx->p_status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
     CK(cudaEventRecord(ctx->ev[3], st), "event");
-    CK(cudaStreamSynchronize(st), "gls");
-    CK(cudaGetLastError(), "gls");
+    if ((rc = finish(ctx, "gls"))) return rc;
     ctx->cv_done = true;
-    record_timing(ctx, L, launches);
+    record_timing(ctx, L, launches, 1);
     if (xtmx) memcpy(xtmx, sums.data(), sizeof(double) * p * p);
     if (xtmy) memcpy(xtmy, sums.data() + p * p, sizeof(double) * p);
     if (std::isnan(sums[0])) return ctx->fail_with(PGPCV_ENUMERIC, "a subset was not positive definite");
@@ -1157,6 +1396,23 @@ int pgpcv_partition_export_test(pgpcv_ctx *ctx, int64_t *test_off, int32_t *test
         CK(cudaMemcpyAsync(test_idx, ctx->test_idx.p, sizeof(int32_t) * ctx->info.n_test, cudaMemcpyDeviceToHost,
                            ctx->stream), "copy test_idx");
     CK(cudaStreamSynchronize(ctx->stream), "export");
+    return PGPCV_OK;
+}
+
+int pgpcv_device_math(pgpcv_ctx *ctx, int32_t fn, int64_t n, const double *x, double *y) {
+    if (!ctx) return PGPCV_EINVAL;
+    if (fn < PGPCV_MATH_EXP_NEG || fn > PGPCV_MATH_RSQRT || n < 0 || (n > 0 && (!x || !y)))
+        return ctx->fail_with(PGPCV_EINVAL, "bad function id, n or NULL array");
+    if (n == 0) return PGPCV_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> dx, dy;
+    CK(dx.ensure(n), "alloc");
+    CK(dy.ensure(n), "alloc");
+    CK(cudaMemcpyAsync(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy");
+    CK(launch_device_math(fn, n, dx.p, dy.p, st), "device math");
+    CK(cudaMemcpyAsync(y, dy.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaStreamSynchronize(st), "device math");
     return PGPCV_OK;
 }
 

@@ -30,7 +30,8 @@ struct CvArgs {
     int32_t out_C;              // output row stride: entry (s, c) at s*out_C + (out_C > 1 ? c : 0)
     int32_t flags;              // kCvPredict | kCvNll
     double *subset_loss;        // [N*out_C] SSPE of the targets (kCvPredict)
-    double *subset_nll;         // [N*out_C] -2 log-likelihood of the training data (kCvNll)
+    double *logdet;             // [N*out_C] sum_i log L_ii (kCvNll), for -2 log L (Eq.2)
+    double *zz;                 // [N*out_C] ||L^{-1} y_T||^2 (kCvNll)
     double *yhat;               // [sum of targets] kriging predictions, or nullptr
     uint8_t *fail;              // [N*out_C] 1 = not positive definite
     // kCvGls (row f4): p covariate rows bordered below y; per-subset core-row sums
@@ -68,6 +69,14 @@ cudaError_t launch_gls_solve(const double *part, const uint8_t *fail, int64_t N,
 cudaError_t launch_gather_rows(int64_t cnt, const int32_t *idx, const double *X, int32_t p, double *out,
                                cudaStream_t st);
 cudaError_t cv_kernel_occupancy(int *blocks_per_sm);
+// zeta dedup: entry (s, c) <- unique-config entry (s, umap[c]) (stride U) where own[s], else
+// 0; with nll: -2 log L_s = k log 2pi + k log sigma2_c + 2 logdet + zz / sigma2_c (Eq.2).
+cudaError_t launch_expand(int64_t N, int32_t C, int32_t U, const int32_t *umap, const uint8_t *own,
+                          const int64_t *train_off, const double *sigma2, const double *u_loss,
+                          const uint8_t *u_fail, const double *u_logdet, const double *u_zz, double *loss,
+                          uint8_t *fail, double *nll, cudaStream_t st);
+// diagnostic: the CV kernel's elementary functions on device arrays (pgpcv_device_math)
+cudaError_t launch_device_math(int32_t fn, int64_t n, const double *x, double *y, cudaStream_t st);
 // out[c] = sum_s vals[s*C + c] over subsets s with mask_off[s+1] > mask_off[s] (all subsets
 // when mask_off is null), in ascending s; NaN (and status[c] = first failing s) on failure.
 cudaError_t launch_reduce(const double *vals, const uint8_t *fail, const int64_t *mask_off, int64_t N,

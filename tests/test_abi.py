@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     lib = pg.load_library()
     for name in _declared_symbols():
         assert hasattr(lib, name), name
-    assert pg.version() == pg.ABI_VERSION == 4
+    assert pg.version() == pg.ABI_VERSION == 5
 
 
 def test_library_is_sm100a_only():
@@ -91,3 +91,22 @@ def test_max_k_constant_matches_binding_and_library():
     hdr = int(re.search(r"#define PGPCV_MAX_K (\d+)", src).group(1))
     internal = open(os.path.join(ROOT, "paper_1912_13132_b200", "csrc", "pgpcv_internal.h")).read()
     assert hdr == pg.MAX_K == int(re.search(r"#define PGPCV_MAX_K_INTERNAL (\d+)", internal).group(1))
+
+
+def test_nccl_library_reuses_the_loaded_copy():
+    """With torch imported, the library binds torch's NCCL (one NCCL per process); the
+    report names the path and version (pgpcv_nccl_library)."""
+    import subprocess
+    import sys
+    code = ("import torch, paper_1912_13132_b200 as pg; print(pg.nccl_library())")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    line = out.stdout.strip()
+    assert "libnccl" in line and "(NCCL 2." in line, line
+    assert "nvidia/nccl" in line, line
+
+
+def test_device_math_rejects_bad_args_without_gpu():
+    lib = pg.load_library()
+    x = np.zeros(4)
+    assert lib.pgpcv_device_math(None, 0, 4, x.ctypes.data, x.ctypes.data) == pg.EINVAL

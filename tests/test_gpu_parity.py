@@ -324,6 +324,14 @@ def test_shard_and_evaluate_argument_rules(ctx, pg):
     with pytest.raises(pg.PgpcvError) as ei:
         ctx.evaluate(w.params, loss=False, subset_loss=False, nll=False, subset_nll=False)
     assert ei.value.code == pg.EINVAL
+    # world > 1 without an ncclUniqueId: EINVAL, and the ctx stays at world 1 (it owns
+    # every subset and runs no collective), so the next evaluation is the world-1 one
+    ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+    with pytest.raises(pg.PgpcvError) as ei:
+        ctx.shard(0, 2, None)
+    assert ei.value.code == pg.EINVAL
+    assert np.array_equal(ctx.cv_loss(w.params).subset_loss, base)
+    assert "NCCL" in pg.nccl_library()
 
 
 def test_partition_boundary_points_bit_exact(ctx, golden_dir):

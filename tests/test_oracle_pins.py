@@ -611,6 +611,32 @@ def test_shell_cap_rules():
         assert len(set(kept) - core) == min(len(full - core), cap)
 
 
+
+def test_shell_cap_hand_worked_golden(golden_dir):
+    """Which shell members the cap keeps (R22), pinned by hand: tests/golden/shell_cap_small.json
+    chooses the seed so that subset 1's keys are SplitMix64's published reference outputs
+    (Vigna, seed 0: outputs 1-3), so the kept sets for caps 3, 2, 1, 0 follow by sorting
+    three known numbers.  Pins: smallest keys are kept, the key index is s*2^32 + p + 1,
+    the core is kept whole and a shell within the cap is untouched."""
+    import json
+    g = json.load(open(os.path.join(golden_dir, "shell_cap_small.json")))
+    pts = np.array(g["points"])
+    x, y, role = pts[:, 0], pts[:, 1], pts[:, 2].astype(np.uint8)
+    rects = np.array(g["rects"])
+    part = oracle.partition_rects(x, y, role, g["domain"], rects, g["delta"])
+    for s in range(2):
+        assert part.train(s).tolist() == g["train_uncapped"][s]
+        assert part.val(s).tolist() == g["val"][s]
+    gamma = 0x9e3779b97f4a7c15
+    for p, key in g["keys_subset1"].items():  # the golden's key derivation, checked
+        assert oracle.splitmix64(g["seed"], (1 << 32) + int(p) + 1) == int(key, 16)
+        assert (g["seed"] + ((1 << 32) + int(p) + 1) * gamma) % (1 << 64) == (int(p) + 1) * gamma % (1 << 64)
+    for cap, lists in g["capped"].items():
+        capped = oracle.cap_shells(part, x, y, g["domain"], int(cap), g["seed"])
+        for s in range(2):
+            assert capped.train(s).tolist() == lists[s], (cap, s)
+
+
 # ----------------------------------------------------------------- row f4: GLS
 
 def _gls_setup(seed, n, depth, delta):

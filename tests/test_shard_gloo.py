@@ -1,7 +1,8 @@
 """Multi-rank host logic of the sharded path on CPU (world_size 2, gloo, 127.0.0.1).
 
-pgpcv_shard assigns whole subsets to ranks by LPT on k^3 (the library's pgpcv_lpt_assign,
-host-only) and the combine step (Alg.1 line 9) all-reduces either the per-config
+After pgpcv_shard every CV evaluation assigns the whole subsets it factors (those with
+validation data) to ranks by LPT on k^3 (the library's pgpcv_lpt_assign, host-only, over
+those subsets in ascending id) and the combine step (Alg.1 line 9) all-reduces either the per-config
 loss vector or the per-subset array (each entry with one owner).  Here each rank computes
 its owned subsets with the CPU oracle and the same two all-reduces run over gloo; the
 result must equal the single-process evaluation (bit-exact for the per-subset array)."""
@@ -39,8 +40,9 @@ def _worker(rank, world, port, out_dir):
     w = _data()
     part = oracle.partition(w.x, w.y, w.role, w.domain, w.kx, w.ky, w.delta)
     k, m = part.k().astype(np.float64), part.m()
-    cost = np.where(m > 0, k ** 3, 0.0)
-    owner = pg.lpt_assign(cost, world)  # the C ABI's host-only LPT rule
+    ids = np.nonzero(m > 0)[0]
+    owner = np.full(part.n_subsets, -1, np.int32)
+    owner[ids] = pg.lpt_assign(k[ids] ** 3, world)  # the C ABI's host-only LPT rule
     mine = np.nonzero((owner == rank) & (m > 0))[0]
     params = w.params[[0, 37, 74]]
     rep = oracle.cv_loss(w.x, w.y, w.value, part, params, subsets=mine, threads=2)
