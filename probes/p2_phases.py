@@ -1,6 +1,7 @@
 """P2 -- where the cv_kernel's time goes: runs one c5 (or c6) configuration through the
 diagnostic build libpgpcv_phases.so (-DPGPCV_PHASE_PROFILE: thread 0 of every CTA
-attributes its clock64() time to 8 phases) and prints the phase shares as JSON."""
+attributes its clock64() time to 15 phases) and prints the phase shares per kernel variant
+as JSON.  Usage: python probes/p2_phases.py [c2..c6] [lib]  (PGPCV_SMALL_K selects the split)."""
 import json
 import os
 import re
@@ -38,14 +39,17 @@ if not os.path.exists(lib):  # the diagnostic build (not part of __graft_entry__
     _build.build(force=True, defines=["PGPCV_PHASE_PROFILE"], out=lib)
 env = dict(os.environ, PGPCV_LIB=lib)
 r = subprocess.run([sys.executable, __file__, "child", wname], env=env, capture_output=True, text=True)
-m = re.search(r"PGPCV_PHASES (\{.*\})", r.stderr)
+ms = re.findall(r"PGPCV_PHASES (\{.*\})", r.stderr)
 t = re.search(r"TIMING (\{.*\})", r.stdout)
-if not m:
+if not ms:
     sys.stderr.write(r.stdout + r.stderr)
     sys.exit(1)
-d = json.loads(m.group(1))
-cyc = d["cycles"]
-tot = sum(cyc)
-out = {"workload": wname, "lib": os.path.basename(lib), "slots": d["slots"], "timing": json.loads(t.group(1)) if t else None,
-       "share": {n: round(c / tot, 4) for n, c in zip(NAMES, cyc)}}
+out = {"workload": wname, "lib": os.path.basename(lib), "timing": json.loads(t.group(1)) if t else None,
+       "variants": {}}
+for m in ms:  # one line per kernel variant launched (0 large, 1 small)
+    d = json.loads(m)
+    cyc = d["cycles"]
+    tot = sum(cyc)
+    out["variants"][{0: "large", 1: "small"}.get(d.get("variant", 0))] = {
+        "slots": d["slots"], "share": {n: round(c / tot, 4) for n, c in zip(NAMES, cyc)}}
 print(json.dumps(out))

@@ -31,5 +31,7 @@ case "$job" in
     timeout 2400 ncu --set full --import-source on --clock-control none -k regex:cv_kernel -c 1 \
       -o gpurun_out/prof_$tag python bench.py --steps 1 --warmup 0 --configs-per-step 1 --no-cpu-baseline "$@" \
       > gpurun_out/ncu_full_$tag.log 2>&1 ;;
+  phases)
+    timeout 900 python probes/p2_phases.py "$1" > gpurun_out/p2_$1_${2:-default}.json 2> gpurun_out/p2_$1_${2:-default}.err ;;
   *) echo "unknown job $job"; exit 2 ;;
 esac
