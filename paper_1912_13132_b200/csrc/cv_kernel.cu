@@ -60,30 +60,43 @@
 namespace pgpcv {
 namespace {
 
-constexpr int MT = kMT;
-constexpr int NB = kNB;
-constexpr int NT = kThreads;
-constexpr int NWARP = NT / 32;
 constexpr int KC = 16;       // = the column-group width of the factor layout
-constexpr int STAGES = 3;
 #ifndef PGPCV_PFD
 #define PGPCV_PFD 4
 #endif
 constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (chunks)
-constexpr int BS = NB + 4;   // 68 doubles = 136 words == 8 (mod 32): Linv^T rows
-constexpr int LJS = NB + 1;  // 65: row stride of the diagonal block in SMEM
-constexpr int A_STAGE = MT * KC;                         // 2,048 doubles (16 KB)
-constexpr int B_STAGE = NB * KC;                         // 1,024 doubles (8 KB)
-constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE);  // 9,216 doubles
-constexpr int BT_DBL = NB * BS;                          // Linv^T tile
-constexpr int COL_DBL = 3 * NB;                          // block-column x, y, value
-constexpr int MISC_DBL = 2 * NB + NWARP + 64;            // pivots, reciprocals, warp partials, exp table
-constexpr size_t SMEM_BYTES = sizeof(double) * (STAGE_DBL + BT_DBL + COL_DBL + MISC_DBL);
-static_assert(2 * NB * LJS <= STAGE_DBL, "diagonal block and its inverse must fit in the stage buffers");
-static_assert(NB * LJS <= BT_DBL, "back-substitution block must fit in the Linv buffer");
-static_assert(SMEM_BYTES <= 115712, "two CTAs per SM");
-static_assert((BS * 2) % 32 == 8, "fragment-load stride of Linv^T");
-static_assert(MT == 16 * NWARP && NB == 64, "each warp owns 16 rows x 64 columns");
+
+// Kernel geometry.  Two instantiations:
+//   Geo<128, 64, 2>: the large-subset kernel -- 8 warps, row tiles of MT = 128, block
+//     columns of NB = 64, two CTAs per SM (111 KB SMEM each);
+//   Geo<64, 32, 4>:  the small-subset kernel -- 4 warps, MT = 64, NB = 32, four CTAs per SM
+//     (47 KB each): at k of a few hundred the per-item critical path (the diagonal blocks'
+//     pivot chain, the TRSM, the back-substitution) dominates, and twice the items in
+//     flight per SM hide it; its operands stream at 5.3 instead of 10.7 flop/B.
+// Each warp owns 16 full rows x NB columns of a row tile.
+template <int MT_, int NB_, int MINB_>
+struct Geo {
+    static constexpr int MT = MT_, NB = NB_, MINB = MINB_;
+    static constexpr int NWARP = MT / 16, NT = 32 * NWARP;
+    static constexpr int STAGES = 3;
+    static constexpr int BS = NB + 4;   // Linv^T row stride: 2 BS == 8 (mod 32) words, conflict-free fragments
+    static constexpr int LJS = NB + 1;  // row stride of the diagonal block in SMEM
+    static constexpr int A_STAGE = MT * KC;
+    static constexpr int B_STAGE = NB * KC;
+    static constexpr int STAGE_DBL = STAGES * (A_STAGE + B_STAGE);
+    static constexpr int BT_DBL = NB * BS;                  // Linv^T tile
+    static constexpr int COL_DBL = 3 * NB;                  // block-column x, y, value
+    static constexpr int MISC_DBL = 2 * NB + NWARP + 64;    // pivots, warp partials, exp table
+    static constexpr size_t SMEM_BYTES = sizeof(double) * (STAGE_DBL + BT_DBL + COL_DBL + MISC_DBL);
+    static constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));
+    static_assert(2 * NB * LJS <= STAGE_DBL, "diagonal block and its inverse must fit in the stage buffers");
+    static_assert(NB * LJS <= BT_DBL, "back-substitution block must fit in the Linv buffer");
+    static_assert(SMEM_BYTES * MINB <= 232448 - MINB * 1024, "MINB CTAs per SM");
+    static_assert((BS * 2) % 32 == 8, "fragment-load stride of Linv^T");
+    static_assert(MT == 16 * NWARP && (NB == 64 || NB == 32) && MT >= NB, "warp tile 16 x NB");
+};
+using GeoLarge = Geo<kMT, kNB, 2>;
+using GeoSmall = Geo<kMTSmall, kNBSmall, 4>;
 
 // ---------------------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -168,8 +181,6 @@ constexpr int kTimelineLen = 1 << 15;
 // factorization (warp 0), 14 trailing updates and their barriers
 constexpr int kPhases = 15;
 
-constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));  // 24,576 B
-
 // Packed lower-triangular storage: column group q (columns 16q..16q+15) is only ever read or
 // written at rows >= 16q, so it stores rows 16q..ld-1; groups follow each other.  Row r of
 // group q starts at (gbase(q) + r) * 16 with gbase(q) = sum_{q'<q} (ld - 16q') - 16q.
@@ -192,34 +203,51 @@ __device__ __forceinline__ const double *lchunk(const double *L, int64_t ld, int
 // rows r0..r0+MT-1 (A) and j0..j0+NB-1 (B) of column group kk/16.  Rows past the matrix
 // are copied as whatever the workspace holds; they only reach discarded outputs (see the
 // masking of acc after the update).  Chunk n + PFD is prefetched into L2.
+template <class G>
 __device__ __forceinline__ void issue_chunk(uint32_t n, double *stage, uint64_t *full, uint64_t *empty,
                                             const double *L, int64_t ld, int r0, int j0, int kk) {
-    const int sidx = n % STAGES;
-    const uint32_t use = n / STAGES;
+    const int sidx = n % G::STAGES;
+    const uint32_t use = n / G::STAGES;
     if (use > 0) mbar_wait(&empty[sidx], (use - 1) & 1);
-    double *sb = stage + sidx * (A_STAGE + B_STAGE);
-    mbar_expect_tx(&full[sidx], STAGE_BYTES);
-    bulk_g2s(sb, lchunk(L, ld, kk / KC, r0), MT * KC * sizeof(double), &full[sidx]);
-    bulk_g2s(sb + A_STAGE, lchunk(L, ld, kk / KC, j0), NB * KC * sizeof(double), &full[sidx]);
+    double *sb = stage + sidx * (G::A_STAGE + G::B_STAGE);
+    mbar_expect_tx(&full[sidx], G::STAGE_BYTES);
+    bulk_g2s(sb, lchunk(L, ld, kk / KC, r0), G::MT * KC * sizeof(double), &full[sidx]);
+    bulk_g2s(sb + G::A_STAGE, lchunk(L, ld, kk / KC, j0), G::NB * KC * sizeof(double), &full[sidx]);
 }
+template <class G>
 __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int r0, int j0, int kk) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lchunk(L, ld, kk / KC, r0)),
-                 "r"((unsigned)(MT * KC * sizeof(double)))
+                 "r"((unsigned)(G::MT * KC * sizeof(double)))
                  : "memory");
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lchunk(L, ld, kk / KC, j0)),
-                 "r"((unsigned)(NB * KC * sizeof(double)))
+                 "r"((unsigned)(G::NB * KC * sizeof(double)))
                  : "memory");
 }
+// Column of the i-th operand chunk of a tile: ascending on even row tiles, descending on
+// odd ones (a boustrophedon over the k-chunks), so a tile starts with the B-panel chunks
+// the previous tile of the same block column read last -- still in L2.
+#ifndef PGPCV_SNAKE
+#define PGPCV_SNAKE 1
+#endif
+__device__ __forceinline__ int chunk_col(int i, int nk, bool rev) { return (PGPCV_SNAKE && rev ? nk - 1 - i : i) * KC; }
 // Tile prologue: SMEM chunks 0..STAGES-2 and L2 prefetches of the next PFD chunks.
+template <class G>
 __device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage, uint64_t *full,
                                               uint64_t *empty, const double *L, int64_t ld, int r0,
-                                              int j0) {
+                                              int j0, bool rev) {
     fence_proxy_async();
-    for (int i = 0; i < min(STAGES - 1, nk); ++i) issue_chunk(pc + i, stage, full, empty, L, ld, r0, j0, i * KC);
-    for (int i = STAGES - 1; i < min(STAGES - 1 + PFD, nk); ++i) prefetch_chunk(L, ld, r0, j0, i * KC);
+    for (int i = 0; i < min(G::STAGES - 1, nk); ++i)
+        issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev));
+    for (int i = G::STAGES - 1; i < min(G::STAGES - 1 + PFD, nk); ++i)
+        prefetch_chunk<G>(L, ld, r0, j0, chunk_col(i, nk, rev));
 }
 
-__global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
+template <class G>
+__global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
+    constexpr int MT = G::MT, NB = G::NB, NT = G::NT, NWARP = G::NWARP, STAGES = G::STAGES;
+    constexpr int BS = G::BS, LJS = G::LJS, A_STAGE = G::A_STAGE, B_STAGE = G::B_STAGE;
+    constexpr int STAGE_DBL = G::STAGE_DBL, BT_DBL = G::BT_DBL;
+    constexpr int NJ = NB / 8;  // 8-column fragments per warp row block
     extern __shared__ __align__(128) double smem[];
     double *stage = smem;
     double *LJ = smem;                  // diagonal block [r][c], aliases the stages
@@ -329,14 +357,25 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
             // before the last barrier) are read next by bulk copies (async proxy); the
             // stage memory was last touched by generic accesses (LJ, alpha).
             PH(0);
-            if (tid == 0) tile_prologue(pc, nk, stage, full, empty, L, ld, j0, j0);
+            if (tid == 0) tile_prologue<G>(pc, nk, stage, full, empty, L, ld, j0, j0, false);
             __syncwarp();
             __syncthreads();  // cx/cy/cv visible
             PH(1);
             for (int rt = 0; rt < ntiles; ++rt) {
                 const int r0 = j0 + rt * MT;
                 const int rbase = r0 + warp * 16;  // this warp's first row
-                double acc[2][8][2];
+                double acc[2][NJ][2];
+
+                const bool live = rbase <= kb;  // this warp holds at least one row of the matrix
+                // In tile 0 the warps holding rows of the diagonal block need only the
+                // column fragments at or below the diagonal (j <= 2 warp + 1): the upper part
+                // of L_jj is never read, so neither its entries nor its DMMAs are computed
+                // (rt == 0: warp-uniform).  A warp whose rows all lie in the padding of the
+                // last tile computes nothing.
+#ifndef PGPCV_DIAGSKIP
+#define PGPCV_DIAGSKIP 1
+#endif
+                const int jlim = !live ? 0 : (PGPCV_DIAGSKIP && rt == 0 && warp * 16 < NB) ? min(NJ, 2 * warp + 2) : NJ;
 
                 // acc = -A[r0:r0+MT, j0:j0+NB] (Eq.3 second line), generated while
                 // the first operand chunks of the tile are in flight.
@@ -352,27 +391,42 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     // interleave); the special entries by selects.  (Generating the next
                     // tile's entries inside the update loop instead was measured 5 % slower:
                     // the exp chains then compete with the DMMA stream of the same warp.)
+                    auto gen = [&](int i, int j, int e) {
+                        const int r = rbase + i * 8 + g;
+                        const int nl = j * 8 + 2 * t + e;
+                        const int cc = j0 + nl;
+                        const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
+                        double v = -exp_neg(sqrt_nb(dx * dx + dy * dy) * ninv, etab);
+                        v = r == cc ? -(1.0 + lam) : v;                 // exp(0) + lambda
+                        v = r == k ? -cv[nl] : v;                       // bordered y_T
+                        v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
+                        acc[i][j][e] = v;
+                    };
+                    if (jlim == NJ) {
 #pragma unroll
-                    for (int i = 0; i < 2; ++i)
+                        for (int i = 0; i < 2; ++i)
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
+                            for (int j = 0; j < NJ; ++j)
 #pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int r = rbase + i * 8 + g;
-                                const int nl = j * 8 + 2 * t + e;
-                                const int cc = j0 + nl;
-                                const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
-                                double v = -exp_neg(sqrt_nb(dx * dx + dy * dy) * ninv, etab);
-                                v = r == cc ? -(1.0 + lam) : v;                 // exp(0) + lambda
-                                v = r == k ? -cv[nl] : v;                       // bordered y_T
-                                v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
-                                acc[i][j][e] = v;
-                            }
+                                for (int e = 0; e < 2; ++e) gen(i, j, e);
+                    } else {  // diagonal-block warps of tile 0, or a padding warp
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+#pragma unroll
+                            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    if (j < jlim)
+                                        gen(i, j, e);
+                                    else
+                                        acc[i][j][e] = 0.0;
+                                }
+                    }
                     if (np > 0) {  // bordered covariate rows (GLS, row f4)
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
 #pragma unroll
-                            for (int j = 0; j < 8; ++j)
+                            for (int j = 0; j < NJ; ++j)
 #pragma unroll
                                 for (int e = 0; e < 2; ++e) {
                                     const int r = rbase + i * 8 + g;
@@ -386,15 +440,14 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 PH(2);
                 // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
-                const bool live = rbase <= kb;  // this warp holds at least one row of the matrix
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
                     if (tid == 0) {
                         if (kc + STAGES - 1 < nk)
-                            issue_chunk(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
-                                        (kc + STAGES - 1) * KC);
+                            issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
+                                           chunk_col(kc + STAGES - 1, nk, rt & 1));
                         if (kc + STAGES - 1 + PFD < nk)
-                            prefetch_chunk(L, ld, r0, j0, (kc + STAGES - 1 + PFD) * KC);
+                            prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + PFD, nk, rt & 1));
                     }
                     PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
@@ -405,19 +458,35 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                     const double *bp = As + A_STAGE + g * KC + t;
                     // A warp whose 16 rows all lie below the last bordered row (the padding
                     // of a tile that overhangs the matrix) issues no DMMA (warp-uniform).
-                    if (live)
+                    if (jlim == NJ) {
 #pragma unroll
-                    for (int k4 = 0; k4 < KC / 4; ++k4) {
-                        const int o = (k4 << 2) ^ sw;
-                        double af[2], bf[8];
-                        af[0] = ap[o];
-                        af[1] = ap[8 * KC + o];
+                        for (int k4 = 0; k4 < KC / 4; ++k4) {
+                            const int o = (k4 << 2) ^ sw;
+                            double af[2], bf[NJ];
+                            af[0] = ap[o];
+                            af[1] = ap[8 * KC + o];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * KC + o];
+                            for (int j = 0; j < NJ; ++j) bf[j] = bp[j * 8 * KC + o];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
+                            for (int j = 0; j < NJ; ++j)
 #pragma unroll
-                            for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
+                                for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
+                        }
+                    } else if (jlim > 0) {  // tile 0, warps on the diagonal block: lower part only
+#pragma unroll
+                        for (int k4 = 0; k4 < KC / 4; ++k4) {
+                            const int o = (k4 << 2) ^ sw;
+                            double af[2];
+                            af[0] = ap[o];
+                            af[1] = ap[8 * KC + o];
+#pragma unroll
+                            for (int j = 0; j < NJ; ++j)
+                                if (j < jlim) {
+                                    const double bfj = bp[j * 8 * KC + o];
+#pragma unroll
+                                    for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bfj);
+                                }
+                        }
                     }
                     // Release the stage: this warp's generic-proxy reads of it must be
                     // ordered before the async-proxy bulk copy that will refill it (the
@@ -432,7 +501,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 // Columns past the matrix (last block column) came from rows of the
                 // workspace beyond the factor: force C = 0 there (Linv^T is 0 there too).
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+                for (int j = 0; j < NJ; ++j)
 #pragma unroll
                     for (int e = 0; e < 2; ++e)
                         if (j0 + j * 8 + 2 * t + e >= k) acc[0][j][e] = acc[1][j][e] = 0.0;
@@ -445,7 +514,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
 #pragma unroll
-                            for (int j = 0; j < 8; ++j)
+                            for (int j = 0; j < NJ; ++j)
 #pragma unroll
                                 for (int e = 0; e < 2; ++e) {
                                     const int rl = warp * 16 + i * 8 + g;
@@ -474,7 +543,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 #pragma unroll
                             for (int c2 = 0; c2 < 8; ++c2) {
                                 va[c2] = (ra < jw && c2 < pw) ? LJ[ra * LJS + p0 + c2] : 0.0;
-                                vb[c2] = (rb < jw && c2 < pw) ? LJ[rb * LJS + p0 + c2] : 0.0;
+                                vb[c2] = (NB > 32 && rb < jw && c2 < pw) ? LJ[rb * LJS + p0 + c2] : 0.0;
                             }
                             bool bad = false;
                             double rinv[8];
@@ -513,7 +582,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 #pragma unroll
                             for (int c2 = 0; c2 < 8; ++c2) {
                                 if (c2 < pw && ra < jw && lane >= c2) LJ[ra * LJS + p0 + c2] = va[c2];
-                                if (c2 < pw && rb < jw) LJ[rb * LJS + p0 + c2] = vb[c2];
+                                if (NB > 32 && c2 < pw && rb < jw) LJ[rb * LJS + p0 + c2] = vb[c2];
                             }
                             if (bad && lane == 0) s_fail = 1;
                             __syncwarp();
@@ -526,7 +595,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 #pragma unroll
                                 for (int i = 0; i < 8; ++i) {
                                     w0[i] = i < pw ? RI[(p0 + i) * LJS + lane] : 0.0;
-                                    w1[i] = i < pw ? RI[(p0 + i) * LJS + lane + 32] : 0.0;
+                                    w1[i] = (NB > 32 && i < pw) ? RI[(p0 + i) * LJS + lane + 32] : 0.0;
                                 }
 #pragma unroll
                                 for (int i = 0; i < 8; ++i) {
@@ -542,7 +611,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 #pragma unroll
                                 for (int i = 0; i < 8; ++i) {
                                     if (i < pw && lane <= p0 + i) RI[(p0 + i) * LJS + lane] = w0[i];
-                                    if (i < pw && lane + 32 <= p0 + i) RI[(p0 + i) * LJS + lane + 32] = w1[i];
+                                    if (NB > 32 && i < pw && lane + 32 <= p0 + i) RI[(p0 + i) * LJS + lane + 32] = w1[i];
                                 }
                             }
                         }
@@ -626,7 +695,8 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
 
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
-                if (rt + 1 < ntiles && tid == 0) tile_prologue(pc, nk, stage, full, empty, L, ld, r0 + MT, j0);
+                if (rt + 1 < ntiles && tid == 0)
+                    tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1);
                 __syncwarp();
 
                 // X = C . Linv^T = -(acc . Linv^T) (triangular solve against L_jj^T as a
@@ -638,7 +708,7 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                 const int src_lo = (g << 2) + (t >> 1);
                 const bool odd = t & 1;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NB / 32; ++h) {
                     double xo[2][4][2];
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
@@ -764,8 +834,10 @@ __global__ void __launch_bounds__(NT, 2) cv_kernel(CvArgs a) {
                         p1 += __ldcg(row + (((c0 + 1) & 15) ^ sw)) * ar;
                     }
                 }
-                part2[warp * NB + c0] = p0;
-                part2[warp * NB + c0 + 1] = p1;
+                if (c0 < NB) {
+                    part2[warp * NB + c0] = p0;
+                    part2[warp * NB + c0 + 1] = p1;
+                }
             }
             __syncthreads();
             if (tid < jw) {
@@ -1000,32 +1072,47 @@ cudaError_t launch_gather_rows(int64_t cnt, const int32_t *idx, const double *X,
     return cudaGetLastError();
 }
 
-size_t cv_kernel_smem_bytes() { return SMEM_BYTES; }
-int cv_kernel_max_k() { return PGPCV_MAX_K_INTERNAL; }  // = PGPCV_MAX_K (include/pgpcv.h)
-size_t cv_kernel_slot_doubles(int64_t kmax, int extra_rows) {
-    // the packed factor + alpha when it does not fit in SMEM + MT x 16: a bulk copy of the
-    // last group's row tile may read past the factor's end.  Rounded to 256 B so
-    // every slot base keeps the alignment bulk copies need.
+template <class G>
+size_t slot_doubles(int64_t kmax, int extra_rows) {
+    // the packed factor + alpha when it does not fit in SMEM + the inverse of every diagonal
+    // block + MT x 16: a bulk copy of the last group's row tile may read past the factor's
+    // end.  Rounded to 256 B so every slot base keeps the alignment bulk copies need.
     const int64_t groups = (kmax + KC - 1) / KC;
     const size_t d = (size_t)factor_doubles(factor_ld(kmax + extra_rows), groups > 0 ? groups : 1) +
-                     (size_t)((kmax + 31) / 32) * 32 + (size_t)((kmax + NB - 1) / NB) * NB * NB +
-                     (size_t)MT * KC;
+                     (size_t)((kmax + 31) / 32) * 32 + (size_t)((kmax + G::NB - 1) / G::NB) * G::NB * G::NB +
+                     (size_t)G::MT * KC;
     return (d + 31) / 32 * 32;
 }
 
-cudaError_t cv_kernel_occupancy(int *blocks_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(cv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM_BYTES);
+template <class G>
+cudaError_t occupancy(int *blocks_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(cv_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)G::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, cv_kernel, NT, SMEM_BYTES);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, cv_kernel<G>, G::NT, G::SMEM_BYTES);
 }
 
-cudaError_t launch_cv_kernel(const CvArgs &a, int grid, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(cv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM_BYTES);
+template <class G>
+cudaError_t launch(const CvArgs &a, int grid, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(cv_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)G::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    cv_kernel<<<grid, NT, SMEM_BYTES, st>>>(a);
+    cv_kernel<G><<<grid, G::NT, G::SMEM_BYTES, st>>>(a);
     return cudaGetLastError();
+}
+
+size_t cv_kernel_smem_bytes(int variant) {
+    return variant == kCvSmall ? GeoSmall::SMEM_BYTES : GeoLarge::SMEM_BYTES;
+}
+int cv_kernel_max_k() { return PGPCV_MAX_K_INTERNAL; }  // = PGPCV_MAX_K (include/pgpcv.h)
+size_t cv_kernel_slot_doubles(int variant, int64_t kmax, int extra_rows) {
+    return variant == kCvSmall ? slot_doubles<GeoSmall>(kmax, extra_rows) : slot_doubles<GeoLarge>(kmax, extra_rows);
+}
+cudaError_t cv_kernel_occupancy(int variant, int *blocks_per_sm) {
+    return variant == kCvSmall ? occupancy<GeoSmall>(blocks_per_sm) : occupancy<GeoLarge>(blocks_per_sm);
+}
+cudaError_t launch_cv_kernel(int variant, const CvArgs &a, int grid, cudaStream_t st) {
+    return variant == kCvSmall ? launch<GeoSmall>(a, grid, st) : launch<GeoLarge>(a, grid, st);
 }
 
 cudaError_t launch_expand(int64_t N, int32_t C, int32_t U, const int32_t *umap, const uint8_t *own,

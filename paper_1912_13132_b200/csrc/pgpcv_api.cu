@@ -225,13 +225,16 @@ struct pgpcv_ctx {
     DevBuf<int32_t> p_status;
     // pgpcv_gls
     DevBuf<double> g_X, g_tX, g_part, g_sums, g_beta;
-    DevBuf<unsigned long long> prof;  // diagnostic phase cycles (-DPGPCV_PHASE_PROFILE)
+    DevBuf<unsigned long long> prof, prof2;  // diagnostic phase cycles (-DPGPCV_PHASE_PROFILE)
     DevBuf<unsigned long long> tl;    // diagnostic timeline (-DPGPCV_TIMELINE)
     // pgpcv_select: the last evaluation's device-resident per-subset losses
     int32_t sel_C = 0;
     DevBuf<double> sel_rmspe, sel_local;
     DevBuf<int32_t> sel_best, sel_wins;
-    int blocks_per_sm = 0;
+    int blocks_per_sm[2] = {0, 0};  // resident CTAs per SM of the large / small kernel
+    int64_t small_k = 2048;         // subsets with k <= small_k run on the small kernel (PGPCV_SMALL_K)
+    cudaStream_t aux_stream = nullptr;  // the small kernel's stream when both kernels run
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int sched = 0;  // CvArgs::sched; PGPCV_SCHED overrides (diagnostics)
     pgpcv_timing timing{};
     bool has_timing = false;
@@ -527,11 +530,20 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     if (const char *env = getenv("PGPCV_SCHED")) ctx->sched = atoi(env);
     for (auto &ev : ctx->ev) cudaEventCreate(&ev);
     cudaEventCreateWithFlags(&ctx->ev_sync, cudaEventDisableTiming);
-    if ((e = cv_kernel_occupancy(&ctx->blocks_per_sm)) != cudaSuccess || ctx->blocks_per_sm < 1) {
-        g_create_error = std::string("cv kernel cannot be resident: ") + cudaGetErrorString(e);
+    for (int v = 0; v < 2; ++v)
+        if ((e = cv_kernel_occupancy(v, &ctx->blocks_per_sm[v])) != cudaSuccess || ctx->blocks_per_sm[v] < 1) {
+            g_create_error = std::string("cv kernel cannot be resident: ") + cudaGetErrorString(e);
+            pgpcv_destroy(ctx);
+            return PGPCV_ECUDA;
+        }
+    if ((e = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking)) != cudaSuccess) {
+        g_create_error = cudaGetErrorString(e);
         pgpcv_destroy(ctx);
         return PGPCV_ECUDA;
     }
+    cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+    if (const char *env = getenv("PGPCV_SMALL_K")) ctx->small_k = atoll(env);
     *out = ctx;
     return PGPCV_OK;
 }
@@ -544,6 +556,9 @@ void pgpcv_destroy(pgpcv_ctx *ctx) {
     for (auto &ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
@@ -774,19 +789,34 @@ struct CvLaunch {
     int slots = 0;
 };
 
+// One batched evaluation of `items` (subset, config) in LPT order (descending k): items
+// with k > small_k run on the large-subset kernel, the rest on the small-subset kernel
+// (cv_kernel.cu, Geo<128,64,2> / Geo<64,32,4>), the two launched on forked streams so the
+// small kernel's CTAs fill SMs as the large kernel's persistent CTAs drain.  Each kernel
+// gets one factor slot per resident CTA, sized for its largest subset.  Records the span
+// of the launches on ctx->ev[1..2].  Outputs are device arrays of stride out_C (CvArgs).
 int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     cudaStream_t st = ctx->stream;
+    auto kof = [&](const int2 &it) { return ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]; };
     // LPT: descending k (stable, so ties keep ascending subset / config order)
-    std::stable_sort(L.items.begin(), L.items.end(), [&](const int2 &a, const int2 &b) {
-        return ctx->h_train_off[a.x + 1] - ctx->h_train_off[a.x] > ctx->h_train_off[b.x + 1] - ctx->h_train_off[b.x];
-    });
+    std::stable_sort(L.items.begin(), L.items.end(), [&](const int2 &a, const int2 &b) { return kof(a) > kof(b); });
     int64_t kmax = 0;
-    for (const int2 &it : L.items) kmax = std::max(kmax, ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]);
+    for (const int2 &it : L.items) kmax = std::max(kmax, kof(it));
     if (kmax > cv_kernel_max_k())
         return ctx->fail_with(PGPCV_EINVAL, "a subset has %lld training points (max %d)", (long long)kmax,
                               cv_kernel_max_k());
     const int64_t n_items = (int64_t)L.items.size();
     if (n_items >= ((int64_t)1 << 31)) return ctx->fail_with(PGPCV_EINVAL, "too many work items");
+    // split point: items [0, n_large) are large, [n_large, n_items) small
+    int64_t n_large = 0;
+    while (n_large < n_items && kof(L.items[n_large]) > ctx->small_k) ++n_large;
+    struct Part {
+        int variant;
+        int64_t first, count, kmax;
+        int slots = 0;
+        size_t stride = 0, offset = 0;
+    } parts[2] = {{kCvLarge, 0, n_large, n_large ? kof(L.items[0]) : 0},
+                  {kCvSmall, n_large, n_items - n_large, n_items > n_large ? kof(L.items[n_large]) : 0}};
     std::vector<double> hp(3 * (size_t)L.C);
     for (int c = 0; c < L.C; ++c) {
         hp[3 * c] = L.params[c].range;
@@ -795,29 +825,46 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     }
     CK(ctx->params.ensure(3 * (size_t)L.C), "alloc params");
     CK(ctx->items.ensure(std::max<int64_t>(n_items, 1)), "alloc items");
-    CK(ctx->counter.ensure(1 + kMaxSms), "alloc counter");
-    // factor workspace: one (k+1) x k factor per resident CTA
-    int slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm, std::max<int64_t>(n_items, 1));
-    if (const char *env = getenv("PGPCV_MAX_SLOTS")) {  // diagnostics: cap resident CTAs
-        const int cap = atoi(env);
-        if (cap > 0) slots = std::min(slots, cap);
+    CK(ctx->counter.ensure(2 * (1 + kMaxSms)), "alloc counter");
+    // factor workspace: one factor per resident CTA of each kernel
+    int cap = 0;
+    if (const char *env = getenv("PGPCV_MAX_SLOTS")) cap = atoi(env);  // diagnostics: cap resident CTAs
+    size_t total = 0;
+    for (Part &q : parts) {
+        if (!q.count) continue;
+        q.slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm[q.variant], q.count);
+        if (cap > 0) q.slots = std::min(q.slots, cap);
+        q.stride = cv_kernel_slot_doubles(q.variant, q.kmax, L.p);
     }
-    const size_t slot_stride = cv_kernel_slot_doubles(kmax, L.p);
     while (true) {
-        cudaError_t e = ctx->work.ensure((size_t)slots * slot_stride);
+        total = 0;
+        for (Part &q : parts) {
+            q.offset = total;
+            total += (size_t)q.slots * q.stride;
+        }
+        cudaError_t e = ctx->work.ensure(std::max<size_t>(total, 1));
         if (e == cudaSuccess) break;
-        if (slots == 1) return ctx->cuda_fail(e, "alloc factor workspace");
-        slots = std::max(1, slots / 2);
+        Part &big = parts[0].slots * parts[0].stride >= parts[1].slots * parts[1].stride ? parts[0] : parts[1];
+        if (big.slots <= 1) return ctx->cuda_fail(e, "alloc factor workspace");
+        big.slots = std::max(1, big.slots / 2);
     }
-    L.slots = slots;
+    L.slots = parts[0].slots + parts[1].slots;
     CK(cudaMemcpyAsync(ctx->params.p, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, st),
        "copy params");
     if (n_items)
         CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_items, cudaMemcpyHostToDevice, st),
            "copy items");
-    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * (1 + kMaxSms), st), "memset");
+    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * 2 * (1 + kMaxSms), st), "memset");
     CK(cudaEventRecord(ctx->ev[1], st), "event");
-    if (n_items) {
+    const bool both = parts[0].count && parts[1].count;
+    if (both) {  // fork: the small kernel on the auxiliary stream
+        CK(cudaEventRecord(ctx->ev_fork, st), "event");
+        CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_fork, 0), "stream wait");
+    }
+    for (int pi = 0; pi < 2; ++pi) {
+        const Part &q = parts[pi];
+        if (!q.count) continue;
+        cudaStream_t ls = (both && pi == 1) ? ctx->aux_stream : st;
         CvArgs a;
         a.train_off = ctx->train_off.p;
         a.val_off = L.tgt_off;
@@ -829,12 +876,12 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.vv = L.gv;
         a.params = ctx->params.p;
         a.C = L.C;
-        a.items = ctx->items.p;
-        a.n_items = (int32_t)n_items;
-        a.counter = ctx->counter.p;
+        a.items = ctx->items.p + q.first;
+        a.n_items = (int32_t)q.count;
+        a.counter = ctx->counter.p + pi * (1 + kMaxSms);
         a.sched = ctx->sched;
-        a.work = ctx->work.p;
-        a.slot_stride = slot_stride;
+        a.work = ctx->work.p + q.offset;
+        a.slot_stride = q.stride;
         a.out_C = L.out_C;
         a.flags = L.flags;
         a.subset_loss = L.subset_loss;
@@ -850,20 +897,29 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.gls_out = L.gls_out;
         a.prof = nullptr;
 #ifdef PGPCV_PHASE_PROFILE
-        CK(ctx->prof.ensure((size_t)slots * 15), "alloc prof");
-        CK(cudaMemsetAsync(ctx->prof.p, 0, sizeof(unsigned long long) * slots * 15, st), "memset");
-        a.prof = ctx->prof.p;
+        DevBuf<unsigned long long> &prof = pi ? ctx->prof2 : ctx->prof;
+        CK(prof.ensure((size_t)q.slots * 15), "alloc prof");
+        CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * q.slots * 15, ls), "memset");
+        a.prof = prof.p;
 #endif
         a.tl = nullptr;
 #ifdef PGPCV_TIMELINE
-        CK(ctx->tl.ensure((size_t)slots * 32768), "alloc timeline");
-        CK(cudaMemsetAsync(ctx->tl.p, 0, sizeof(unsigned long long) * slots * 32768, st), "memset");
-        a.tl = ctx->tl.p;
+        CK(ctx->tl.ensure((size_t)q.slots * 32768), "alloc timeline");
+        CK(cudaMemsetAsync(ctx->tl.p, 0, sizeof(unsigned long long) * q.slots * 32768, ls), "memset");
+        a.tl = pi == 0 ? ctx->tl.p : nullptr;  // the large kernel's timeline only
 #endif
-        CK(launch_cv_kernel(a, slots, st), "cv kernel launch");
+        CK(launch_cv_kernel(q.variant, a, q.slots, ls), "cv kernel launch");
+        ++L.launches;
+    }
+    if (both) {  // join
+        CK(cudaEventRecord(ctx->ev_join, ctx->aux_stream), "event");
+        CK(cudaStreamWaitEvent(st, ctx->ev_join, 0), "stream wait");
+    }
+    CK(cudaEventRecord(ctx->ev[2], st), "event");
 #ifdef PGPCV_TIMELINE
-        if (const char *path = getenv("PGPCV_TIMELINE_FILE")) {
-            std::vector<unsigned long long> h((size_t)slots * 32768);
+    if (const char *path = getenv("PGPCV_TIMELINE_FILE"))
+        if (parts[0].count) {
+            std::vector<unsigned long long> h((size_t)parts[0].slots * 32768);
             CK(cudaMemcpyAsync(h.data(), ctx->tl.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
                                st), "copy timeline");
             CK(cudaStreamSynchronize(st), "timeline");
@@ -873,23 +929,22 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
             }
         }
 #endif
-        ++L.launches;
 #ifdef PGPCV_PHASE_PROFILE
-        {
-            std::vector<unsigned long long> h((size_t)slots * 15);
-            CK(cudaMemcpyAsync(h.data(), ctx->prof.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
-                               st), "copy prof");
-            CK(cudaStreamSynchronize(st), "prof");
-            double sum[15] = {0};
-            for (int b = 0; b < slots; ++b)
-                for (int i = 0; i < 15; ++i) sum[i] += (double)h[(size_t)b * 15 + i];
-            fprintf(stderr, "PGPCV_PHASES {\"slots\": %d, \"cycles\": [", slots);
-            for (int i = 0; i < 15; ++i) fprintf(stderr, "%s%.6e", i ? ", " : "", sum[i]);
-            fprintf(stderr, "]}\n");
-        }
-#endif
+    for (int pi = 0; pi < 2; ++pi) {
+        const Part &q = parts[pi];
+        if (!q.count) continue;
+        std::vector<unsigned long long> h((size_t)q.slots * 15);
+        CK(cudaMemcpyAsync(h.data(), (pi ? ctx->prof2 : ctx->prof).p, sizeof(unsigned long long) * h.size(),
+                           cudaMemcpyDeviceToHost, st), "copy prof");
+        CK(cudaStreamSynchronize(st), "prof");
+        double sum[15] = {0};
+        for (int b = 0; b < q.slots; ++b)
+            for (int i = 0; i < 15; ++i) sum[i] += (double)h[(size_t)b * 15 + i];
+        fprintf(stderr, "PGPCV_PHASES {\"variant\": %d, \"slots\": %d, \"cycles\": [", q.variant, q.slots);
+        for (int i = 0; i < 15; ++i) fprintf(stderr, "%s%.6e", i ? ", " : "", sum[i]);
+        fprintf(stderr, "]}\n");
     }
-    CK(cudaEventRecord(ctx->ev[2], st), "event");
+#endif
     return PGPCV_OK;
 }
 

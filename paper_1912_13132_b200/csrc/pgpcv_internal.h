@@ -50,17 +50,19 @@ constexpr int32_t kMaxCovariates = 8;
 constexpr int kMaxSms = 256;
 #define PGPCV_MAX_K_INTERNAL 65536  // must equal PGPCV_MAX_K in include/pgpcv.h
 
-// Kernel geometry (see cv_kernel.cu for the derivation).
-constexpr int kMT = 128;        // rows per row tile
-constexpr int kNB = 64;         // block-column width of the left-looking Cholesky
-constexpr int kThreads = 256;   // 8 warps
-size_t cv_kernel_smem_bytes();
+// Kernel geometry (see cv_kernel.cu for the derivation): two variants of the same kernel.
+constexpr int kMT = 128;        // large: rows per row tile (8 warps)
+constexpr int kNB = 64;         // large: block-column width of the left-looking Cholesky
+constexpr int kMTSmall = 64;    // small: 4 warps
+constexpr int kNBSmall = 32;
+constexpr int kCvLarge = 0, kCvSmall = 1;
+size_t cv_kernel_smem_bytes(int variant);
 int cv_kernel_max_k();
-size_t cv_kernel_slot_doubles(int64_t kmax, int extra_rows = 0);  // factor + back-substitution scratch
+size_t cv_kernel_slot_doubles(int variant, int64_t kmax, int extra_rows = 0);  // factor + back-substitution scratch
 // leading dimension (doubles) of a k-point factor: column-major (k+1) x k, +1 bordered row
 __host__ __device__ inline int64_t factor_ld(int64_t k) { return ((k + 1 + 15) / 16) * 16; }
 
-cudaError_t launch_cv_kernel(const CvArgs &a, int grid, cudaStream_t st);
+cudaError_t launch_cv_kernel(int variant, const CvArgs &a, int grid, cudaStream_t st);
 
 // GLS (row f4): out[w] = sum_s part[s*W + w] in ascending s (W = (p+1) p), then
 // beta = A^{-1} b by Gaussian elimination with partial pivoting; *status = 0 ok, 1 singular.
@@ -68,7 +70,7 @@ cudaError_t launch_gls_solve(const double *part, const uint8_t *fail, int64_t N,
                              double *beta, int32_t *status, cudaStream_t st);
 cudaError_t launch_gather_rows(int64_t cnt, const int32_t *idx, const double *X, int32_t p, double *out,
                                cudaStream_t st);
-cudaError_t cv_kernel_occupancy(int *blocks_per_sm);
+cudaError_t cv_kernel_occupancy(int variant, int *blocks_per_sm);
 // zeta dedup: entry (s, c) <- unique-config entry (s, umap[c]) (stride U) where own[s], else
 // 0; with nll: -2 log L_s = k log 2pi + k log sigma2_c + 2 logdet + zz / sigma2_c (Eq.2).
 cudaError_t launch_expand(int64_t N, int32_t C, int32_t U, const int32_t *umap, const uint8_t *own,

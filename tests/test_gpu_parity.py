@@ -162,8 +162,11 @@ def test_c5_full_size_sampled(ctx):
     assert 0.3 < rmspe < 0.5
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 5, 8, 9, 31, 33, 40, 63, 64, 65, 71, 100, 127, 128, 129,
-                               200, 255, 257, 700])
+RAGGED_K = [1, 2, 3, 5, 8, 9, 31, 32, 33, 40, 63, 64, 65, 71, 95, 96, 97, 100, 127, 128, 129,
+            160, 161, 200, 255, 257, 511, 512, 513, 700]
+
+
+@pytest.mark.parametrize("k", RAGGED_K)
 def test_ragged_single_subset(ctx, k):
     """One tile (Eq.7 with N = 1 is Eq.4): k training points not a multiple of the 64-wide
     block or the 128-row tile, m = 7 validation points. The diagonal block's 8-column
@@ -182,6 +185,34 @@ def test_ragged_single_subset(ctx, k):
     ref_part = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
     ref = oracle.cv_loss(x, y, v, ref_part, p, threads=2)
     _assert_close(res.subset_loss, ref.subset_loss)
+
+
+@pytest.mark.parametrize("variant", ["large", "small"])
+def test_ragged_both_kernel_variants(pg, variant):
+    """Every ragged k on each kernel variant (the large 8-warp NB = 64 kernel, and the small
+    4-warp NB = 32 kernel that by default takes k <= 2048), forced with PGPCV_SMALL_K."""
+    os.environ["PGPCV_SMALL_K"] = "0" if variant == "large" else "100000"
+    try:
+        c = pg.Context(0)
+    finally:
+        del os.environ["PGPCV_SMALL_K"]
+    with c:
+        for k in RAGGED_K + [1000, 1025]:
+            m = 5
+            rng = np.random.default_rng(2000 + k)
+            n = k + m
+            x, y = rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+            v = rng.standard_normal(n)
+            role = np.zeros(n, np.uint8)
+            role[rng.permutation(n)[:m]] = 1
+            c.partition(x, y, v, role, (0, 1, 0, 1), 1, 1, 0.0)
+            p = np.array([[0.2, 1.0, 0.05], [0.05, 1.0, 0.3]])
+            res = c.evaluate(p, nll=True, subset_nll=True)
+            ref_part = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
+            ref = oracle.cv_loss(x, y, v, ref_part, p, threads=2)
+            _assert_close(res.subset_loss, ref.subset_loss)
+            _, nll = oracle.neg2loglik_all(x, y, v, ref_part, p, threads=2)
+            _assert_close(res.subset_nll, nll)
 
 
 def test_empty_and_degenerate_subsets(ctx):
