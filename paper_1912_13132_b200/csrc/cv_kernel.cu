@@ -74,9 +74,10 @@ constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (
 //     pivot chain, the TRSM, the back-substitution) dominates, and twice the items in
 //     flight per SM hide it; its operands stream at 5.3 instead of 10.7 flop/B.
 // Each warp owns 16 full rows x NB columns of a row tile.
-template <int MT_, int NB_, int MINB_>
+template <int MT_, int NB_, int MINB_, bool BORDER_>
 struct Geo {
     static constexpr int MT = MT_, NB = NB_, MINB = MINB_;
+    static constexpr bool BORDER = BORDER_;  // bordered prediction compiled in
     static constexpr int NWARP = MT / 16, NT = 32 * NWARP;
     static constexpr int STAGES = 3;
     static constexpr int BS = NB + 4;   // Linv^T row stride: 2 BS == 8 (mod 32) words, conflict-free fragments
@@ -95,8 +96,8 @@ struct Geo {
     static_assert((BS * 2) % 32 == 8, "fragment-load stride of Linv^T");
     static_assert(MT == 16 * NWARP && (NB == 64 || NB == 32) && MT >= NB, "warp tile 16 x NB");
 };
-using GeoLarge = Geo<kMT, kNB, 2>;
-using GeoSmall = Geo<kMTSmall, kNBSmall, 4>;
+using GeoLarge = Geo<kMT, kNB, 2, false>;
+using GeoSmall = Geo<kMTSmall, kNBSmall, 4, true>;
 
 // ---------------------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -329,7 +330,12 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
         const double lam = nugget / sigma2;
         const double ninv = -1.0 / range;
         const int np = (a.flags & kCvGls) ? a.p : 0;  // covariate rows bordered below y (f4)
-        const int kb = k + np;                          // last bordered row
+        // Bordered prediction (border_pred): the m targets' cross-covariance rows b_v are
+        // bordered below y, so the factorization's forward sweep leaves w_v = L^{-1} b_v in
+        // row k+1+v and yhat_v = b_v^T (L L^T)^{-1} y = w_v . z -- no back-substitution.
+        const int nbt = (G::BORDER && a.border_pred && (a.flags & kCvPredict)) ? m : 0;
+        const int kb = k + np + nbt;                    // last bordered row
+        const double *vxi = a.vx + voff, *vyi = a.vy + voff;
         const int64_t ld = factor_ld(kb);
         const int nblk = (k + NB - 1) / NB;
         const int64_t oi = (int64_t)s * a.out_C + (a.out_C > 1 ? c : 0);  // output entry
@@ -367,15 +373,9 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                 double acc[2][NJ][2];
 
                 const bool live = rbase <= kb;  // this warp holds at least one row of the matrix
-                // In tile 0 the warps holding rows of the diagonal block need only the
-                // column fragments at or below the diagonal (j <= 2 warp + 1): the upper part
-                // of L_jj is never read, so neither its entries nor its DMMAs are computed
-                // (rt == 0: warp-uniform).  A warp whose rows all lie in the padding of the
-                // last tile computes nothing.
-#ifndef PGPCV_DIAGSKIP
-#define PGPCV_DIAGSKIP 1
-#endif
-                const int jlim = !live ? 0 : (PGPCV_DIAGSKIP && rt == 0 && warp * 16 < NB) ? min(NJ, 2 * warp + 2) : NJ;
+                // (Skipping the diagonal-block warps' upper fragments in tile 0 -- generation
+                // and DMMAs -- was measured slower at every k: c3 -13 %, c4 -5 %, c5 +0.0 %;
+                // profiles/r02_ab_diagskip.json.  Only whole padding warps skip.)
 
                 // acc = -A[r0:r0+MT, j0:j0+NB] (Eq.3 second line), generated while
                 // the first operand chunks of the tile are in flight.
@@ -384,8 +384,9 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
 #pragma unroll
                     for (int i = 0; i < 2; ++i) {
                         const int r = rbase + i * 8 + g;
-                        rx[i] = r < k ? __ldg(tx + r) : 0.0;
-                        ry[i] = r < k ? __ldg(ty + r) : 0.0;
+                        const bool tgt = G::BORDER && nbt > 0 && r > k && r <= kb;  // bordered target row
+                        rx[i] = r < k ? __ldg(tx + r) : (tgt ? __ldg(vxi + (r - k - 1)) : 0.0);
+                        ry[i] = r < k ? __ldg(ty + r) : (tgt ? __ldg(vyi + (r - k - 1)) : 0.0);
                     }
                     // all 32 entries without branches (independent chains the scheduler can
                     // interleave); the special entries by selects.  (Generating the next
@@ -402,25 +403,18 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                         v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
                         acc[i][j][e] = v;
                     };
-                    if (jlim == NJ) {
+                    if (live) {
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
 #pragma unroll
                             for (int j = 0; j < NJ; ++j)
 #pragma unroll
                                 for (int e = 0; e < 2; ++e) gen(i, j, e);
-                    } else {  // diagonal-block warps of tile 0, or a padding warp
+                    } else {  // a warp of the last tile's padding: nothing to generate
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
 #pragma unroll
-                            for (int j = 0; j < NJ; ++j)
-#pragma unroll
-                                for (int e = 0; e < 2; ++e) {
-                                    if (j < jlim)
-                                        gen(i, j, e);
-                                    else
-                                        acc[i][j][e] = 0.0;
-                                }
+                            for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
                     }
                     if (np > 0) {  // bordered covariate rows (GLS, row f4)
 #pragma unroll
@@ -458,7 +452,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                     const double *bp = As + A_STAGE + g * KC + t;
                     // A warp whose 16 rows all lie below the last bordered row (the padding
                     // of a tile that overhangs the matrix) issues no DMMA (warp-uniform).
-                    if (jlim == NJ) {
+                    if (live) {
 #pragma unroll
                         for (int k4 = 0; k4 < KC / 4; ++k4) {
                             const int o = (k4 << 2) ^ sw;
@@ -471,21 +465,6 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                             for (int j = 0; j < NJ; ++j)
 #pragma unroll
                                 for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
-                        }
-                    } else if (jlim > 0) {  // tile 0, warps on the diagonal block: lower part only
-#pragma unroll
-                        for (int k4 = 0; k4 < KC / 4; ++k4) {
-                            const int o = (k4 << 2) ^ sw;
-                            double af[2];
-                            af[0] = ap[o];
-                            af[1] = ap[8 * KC + o];
-#pragma unroll
-                            for (int j = 0; j < NJ; ++j)
-                                if (j < jlim) {
-                                    const double bfj = bp[j * 8 * KC + o];
-#pragma unroll
-                                    for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bfj);
-                                }
                         }
                     }
                     // Release the stage: this warp's generic-proxy reads of it must be
@@ -902,6 +881,32 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             if (tid == 0) a.fail[oi] = 0;
             fence_proxy_async();
             __syncthreads();
+            continue;
+        }
+        if (G::BORDER && nbt > 0) {
+            // ---------------- bordered prediction (Eq.3, Eq.4): yhat_v = w_v . z ----------
+            double *zs = stage;  // z = L^{-1} y_T, row k of the factor
+            for (int c = tid; c < k; c += NT) zs[c] = __ldcg(L + lidx(ld, k, c));
+            __syncthreads();
+            double part = 0.0;
+            for (int v = warp; v < m; v += NWARP) {
+                double sum = 0.0;
+                for (int c = lane; c < k; c += 32) sum += __ldcg(L + lidx(ld, k + 1 + v, c)) * zs[c];
+                sum = warp_sum(sum);
+                if (a.yhat && lane == 0) a.yhat[voff + v] = sum;
+                const double e = sum - __ldg(a.vv + voff + v);
+                part += e * e;
+            }
+            if (lane == 0) red[warp] = part;
+            fence_proxy_async();  // generic zs accesses before the next item's bulk copies
+            __syncthreads();
+            if (tid == 0) {
+                double l = 0.0;
+                for (int w = 0; w < NWARP; ++w) l += red[w];
+                a.subset_loss[oi] = l;
+                a.fail[oi] = 0;
+            }
+            PH(11);
             continue;
         }
         backsub(k);

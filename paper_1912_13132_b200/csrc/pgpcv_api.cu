@@ -233,6 +233,7 @@ struct pgpcv_ctx {
     DevBuf<int32_t> sel_best, sel_wins;
     int blocks_per_sm[2] = {0, 0};  // resident CTAs per SM of the large / small kernel
     int64_t small_k = 2048;         // subsets with k <= small_k run on the small kernel (PGPCV_SMALL_K)
+    int border_pred = 1;            // small kernel: bordered prediction (PGPCV_BORDER_PRED=0: back-substitute)
     cudaStream_t aux_stream = nullptr;  // the small kernel's stream when both kernels run
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int sched = 0;  // CvArgs::sched; PGPCV_SCHED overrides (diagnostics)
@@ -544,6 +545,7 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
     if (const char *env = getenv("PGPCV_SMALL_K")) ctx->small_k = atoll(env);
+    if (const char *env = getenv("PGPCV_BORDER_PRED")) ctx->border_pred = atoi(env);
     *out = ctx;
     return PGPCV_OK;
 }
@@ -777,7 +779,8 @@ struct CvLaunch {
     int32_t C = 0;
     std::vector<int2> items;
     int32_t out_C = 1;
-    const int64_t *tgt_off = nullptr;
+    const int64_t *tgt_off = nullptr;   // device target offsets
+    const int64_t *h_tgt_off = nullptr; // the same offsets on the host
     const double *gx = nullptr, *gy = nullptr, *gv = nullptr;
     double *subset_loss = nullptr, *logdet = nullptr, *zz = nullptr, *yhat = nullptr;
     uint8_t *fail = nullptr;
@@ -815,8 +818,22 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         int64_t first, count, kmax;
         int slots = 0;
         size_t stride = 0, offset = 0;
+        int border = 0;    // bordered prediction (targets as extra factor rows)
+        int64_t extra = 0; // bordered rows below y: covariates (GLS) or targets
     } parts[2] = {{kCvLarge, 0, n_large, n_large ? kof(L.items[0]) : 0},
                   {kCvSmall, n_large, n_items - n_large, n_items > n_large ? kof(L.items[n_large]) : 0}};
+    // The small kernel predicts by bordering the targets below y (one factorization sweep,
+    // no back-substitution: DESIGN.md section 6) -- m k^2 extra DMMA flops, against a
+    // latency-bound re-read of the whole factor; the large kernel back-substitutes.
+    for (Part &q : parts) {
+        q.extra = L.p;
+        q.border = (L.flags & kCvPredict) && q.variant == kCvSmall && ctx->border_pred;
+        if (q.border)
+            for (int64_t i = q.first; i < q.first + q.count; ++i) {
+                const int s = L.items[i].x;
+                q.extra = std::max<int64_t>(q.extra, L.h_tgt_off[s + 1] - L.h_tgt_off[s]);
+            }
+    }
     std::vector<double> hp(3 * (size_t)L.C);
     for (int c = 0; c < L.C; ++c) {
         hp[3 * c] = L.params[c].range;
@@ -834,7 +851,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         if (!q.count) continue;
         q.slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm[q.variant], q.count);
         if (cap > 0) q.slots = std::min(q.slots, cap);
-        q.stride = cv_kernel_slot_doubles(q.variant, q.kmax, L.p);
+        q.stride = cv_kernel_slot_doubles(q.variant, q.kmax, (int)q.extra);
     }
     while (true) {
         total = 0;
@@ -884,6 +901,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.slot_stride = q.stride;
         a.out_C = L.out_C;
         a.flags = L.flags;
+        a.border_pred = q.border;
         a.subset_loss = L.subset_loss;
         a.logdet = L.logdet;
         a.zz = L.zz;
@@ -1117,6 +1135,7 @@ int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, 
     L.C = U;
     L.out_C = U;
     L.tgt_off = ctx->val_off.p;
+    L.h_tgt_off = ctx->h_val_off.data();
     L.gx = ctx->vx.p;
     L.gy = ctx->vy.p;
     L.gv = ctx->vv.p;
@@ -1306,6 +1325,7 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
     L.C = n_params;
     L.out_C = 1;
     L.tgt_off = test ? ctx->test_off.p : ctx->val_off.p;
+    L.h_tgt_off = hoff.data();
     L.gx = test ? ctx->gx.p : ctx->vx.p;
     L.gy = test ? ctx->gy.p : ctx->vy.p;
     L.gv = test ? ctx->gv.p : ctx->vv.p;
@@ -1381,6 +1401,7 @@ int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, dou
     L.C = 1;
     L.out_C = 1;
     L.tgt_off = ctx->val_off.p;
+    L.h_tgt_off = ctx->h_val_off.data();
     L.gx = ctx->vx.p;
     L.gy = ctx->vy.p;
     L.gv = ctx->vv.p;

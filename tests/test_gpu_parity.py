@@ -215,6 +215,38 @@ def test_ragged_both_kernel_variants(pg, variant):
             _assert_close(res.subset_nll, nll)
 
 
+@pytest.mark.parametrize("border", ["1", "0"])
+def test_bordered_prediction_shapes(pg, border):
+    """The small kernel predicts by bordering the m targets below y (w_v = L^{-1} b_v,
+    yhat_v = w_v . z); many targets spill over several 64-row tiles and block columns.
+    Against the oracle (loss 1e-9 relative, predictions R24), and equal to the
+    back-substitution path (PGPCV_BORDER_PRED=0) within the same bars."""
+    os.environ["PGPCV_BORDER_PRED"] = border
+    try:
+        c = pg.Context(0)
+    finally:
+        del os.environ["PGPCV_BORDER_PRED"]
+    with c:
+        for k, m in [(1, 1), (5, 70), (40, 130), (33, 31), (64, 64), (100, 3), (300, 65), (700, 9)]:
+            rng = np.random.default_rng(3000 + k + m)
+            n = k + m
+            x, y = rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+            v = rng.standard_normal(n)
+            role = np.zeros(n, np.uint8)
+            role[rng.permutation(n)[:m]] = 1
+            c.partition(x, y, v, role, (0, 1, 0, 1), 1, 1, 0.0)
+            p = np.array([[0.2, 1.0, 0.05], [0.07, 1.0, 0.3]])
+            res = c.evaluate(p, nll=True, subset_nll=True)
+            ref_part = oracle.partition(x, y, role, (0, 1, 0, 1), 1, 1, 0.0)
+            ref = oracle.cv_loss(x, y, v, ref_part, p, threads=2)
+            _assert_close(res.subset_loss, ref.subset_loss)
+            for ci in range(2):
+                pr = c.predict(p[ci:ci + 1], target_role=pg.ROLE_VALIDATION)
+                t, w_ = role == 0, role == 1
+                _, yref = oracle.subset_cv(x[t], y[t], v[t], x[w_], y[w_], v[w_], *p[ci], return_yhat=True)
+                assert np.max(np.abs(pr.yhat - yref)) <= 1e-9 * np.sqrt(np.mean(v ** 2)), (k, m, ci)
+
+
 def test_empty_and_degenerate_subsets(ctx):
     """Tiles without validation (loss exactly 0, R10), tiles without training (yhat = 0,
     loss = sum y_V^2, R11), and an all-test tile."""
