@@ -224,6 +224,11 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
                  "r"((unsigned)(G::NB * KC * sizeof(double)))
                  : "memory");
 }
+// Refill protocol: 1 = the last warp to release a stage refills it (round 2); 0 = thread 0
+// issues chunk n + STAGES - 1 at the start of chunk n after waiting for every release.
+#ifndef PGPCV_LAST_REFILLS
+#define PGPCV_LAST_REFILLS 1
+#endif
 // Column of the i-th operand chunk of a tile: ascending on even row tiles, descending on
 // odd ones (a boustrophedon over the k-chunks), so a tile starts with the B-panel chunks
 // the previous tile of the same block column read last -- still in L2.
@@ -237,9 +242,10 @@ __device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage
                                               uint64_t *empty, const double *L, int64_t ld, int r0,
                                               int j0, bool rev) {
     fence_proxy_async();
-    for (int i = 0; i < min(G::STAGES - 1, nk); ++i)
+    constexpr int PRO = PGPCV_LAST_REFILLS ? G::STAGES : G::STAGES - 1;  // chunks in flight at tile start
+    for (int i = 0; i < min(PRO, nk); ++i)
         issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev));
-    for (int i = G::STAGES - 1; i < min(G::STAGES - 1 + PFD, nk); ++i)
+    for (int i = PRO; i < min(PRO + PFD, nk); ++i)
         prefetch_chunk<G>(L, ld, r0, j0, chunk_col(i, nk, rev));
 }
 
@@ -264,6 +270,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
     __shared__ int s_item;
     __shared__ int s_fail;
     __shared__ int s_rank;  // arrival order of this CTA on its SM (sched 1)
+    __shared__ unsigned rel[STAGES];  // releases of each stage's current use (PGPCV_LAST_REFILLS)
 #ifdef PGPCV_PHASE_PROFILE
     __shared__ unsigned long long s_ph[kPhases];
     if (threadIdx.x < kPhases) s_ph[threadIdx.x] = 0;
@@ -279,6 +286,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], NWARP);
+            rel[i] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         unsigned smid;
@@ -333,7 +341,11 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
         // Bordered prediction (border_pred): the m targets' cross-covariance rows b_v are
         // bordered below y, so the factorization's forward sweep leaves w_v = L^{-1} b_v in
         // row k+1+v and yhat_v = b_v^T (L L^T)^{-1} y = w_v . z -- no back-substitution.
-        const int nbt = (G::BORDER && a.border_pred && (a.flags & kCvPredict)) ? m : 0;
+        // Per item: bordering costs m k^2 DMMA flops (3m/k of the factorization); it replaces
+        // the back-substitution only while m <= k / 20 (c3, c4; c2's m/k ~ 0.06 measured
+        // 1.3 % slower bordered).  border_pred 2 borders every item (tests).
+        const int nbt = (G::BORDER && (a.flags & kCvPredict) &&
+                         (a.border_pred == 2 || (a.border_pred == 1 && 20 * m <= k))) ? m : 0;
         const int kb = k + np + nbt;                    // last bordered row
         const double *vxi = a.vx + voff, *vyi = a.vy + voff;
         const int64_t ld = factor_ld(kb);
@@ -436,6 +448,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
+#if !PGPCV_LAST_REFILLS
                     if (tid == 0) {
                         if (kc + STAGES - 1 < nk)
                             issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
@@ -443,6 +456,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                         if (kc + STAGES - 1 + PFD < nk)
                             prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + PFD, nk, rt & 1));
                     }
+#endif
                     PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
                     PH(4);
@@ -473,7 +487,25 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                     // fence stale/partial operands were observed at ~1e-3 of items).
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[n % STAGES]);
+                    if (lane == 0) {
+                        mbar_arrive(&empty[n % STAGES]);
+#if PGPCV_LAST_REFILLS
+                        // The last warp to release the stage refills it with chunk n + STAGES
+                        // at once: no fixed producer thread whose own warp lags behind the
+                        // others (P6: 32.8 -> 34.6 TFLOP/s for the loop alone).
+                        unsigned old;
+                        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                                     : "=r"(old) : "r"(smem_u32(&rel[n % STAGES])) : "memory");
+                        if (old == NWARP - 1) {
+                            rel[n % STAGES] = 0;
+                            if (kc + STAGES < nk)
+                                issue_chunk<G>(n + STAGES, stage, full, empty, L, ld, r0, j0,
+                                               chunk_col(kc + STAGES, nk, rt & 1));
+                            if (kc + STAGES + PFD < nk)
+                                prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES + PFD, nk, rt & 1));
+                        }
+#endif
+                    }
                 }
                 pc += nk;
                 PH(3);

@@ -233,7 +233,8 @@ struct pgpcv_ctx {
     DevBuf<int32_t> sel_best, sel_wins;
     int blocks_per_sm[2] = {0, 0};  // resident CTAs per SM of the large / small kernel
     int64_t small_k = 2048;         // subsets with k <= small_k run on the small kernel (PGPCV_SMALL_K)
-    int border_pred = 1;            // small kernel: bordered prediction (PGPCV_BORDER_PRED=0: back-substitute)
+    int border_pred = 1;            // small kernel: bordered prediction where m <= k/20 (PGPCV_BORDER_PRED:
+                                    // 0 never, 2 always)
     cudaStream_t aux_stream = nullptr;  // the small kernel's stream when both kernels run
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int sched = 0;  // CvArgs::sched; PGPCV_SCHED overrides (diagnostics)
@@ -827,7 +828,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
     // latency-bound re-read of the whole factor; the large kernel back-substitutes.
     for (Part &q : parts) {
         q.extra = L.p;
-        q.border = (L.flags & kCvPredict) && q.variant == kCvSmall && ctx->border_pred;
+        q.border = ((L.flags & kCvPredict) && q.variant == kCvSmall) ? ctx->border_pred : 0;
         if (q.border)
             for (int64_t i = q.first; i < q.first + q.count; ++i) {
                 const int s = L.items[i].x;

@@ -29,7 +29,8 @@ struct CvArgs {
     size_t slot_stride;
     int32_t out_C;              // output row stride: entry (s, c) at s*out_C + (out_C > 1 ? c : 0)
     int32_t flags;              // kCvPredict | kCvNll
-    int32_t border_pred;        // 1: targets bordered below y (prediction without back-substitution)
+    int32_t border_pred;        // targets bordered below y (prediction without back-substitution):
+                                // 0 never, 1 where 20 m <= k, 2 always
     double *subset_loss;        // [N*out_C] SSPE of the targets (kCvPredict)
     double *logdet;             // [N*out_C] sum_i log L_ii (kCvNll), for -2 log L (Eq.2)
     double *zz;                 // [N*out_C] ||L^{-1} y_T||^2 (kCvNll)

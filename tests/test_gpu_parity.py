@@ -215,12 +215,12 @@ def test_ragged_both_kernel_variants(pg, variant):
             _assert_close(res.subset_nll, nll)
 
 
-@pytest.mark.parametrize("border", ["1", "0"])
+@pytest.mark.parametrize("border", ["2", "1", "0"])
 def test_bordered_prediction_shapes(pg, border):
     """The small kernel predicts by bordering the m targets below y (w_v = L^{-1} b_v,
     yhat_v = w_v . z); many targets spill over several 64-row tiles and block columns.
-    Against the oracle (loss 1e-9 relative, predictions R24), and equal to the
-    back-substitution path (PGPCV_BORDER_PRED=0) within the same bars."""
+    Against the oracle (loss 1e-9 relative, predictions R24) with every item bordered
+    (PGPCV_BORDER_PRED=2), the default rule (bordered where m <= k/20) and none (0)."""
     os.environ["PGPCV_BORDER_PRED"] = border
     try:
         c = pg.Context(0)
