@@ -74,12 +74,12 @@ constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (
 //     pivot chain, the TRSM, the back-substitution) dominates, and twice the items in
 //     flight per SM hide it; its operands stream at 5.3 instead of 10.7 flop/B.
 // Each warp owns 16 full rows x NB columns of a row tile.
-template <int MT_, int NB_, int MINB_, bool BORDER_>
+template <int MT_, int NB_, int MINB_, bool BORDER_, int STAGES_ = 3>
 struct Geo {
     static constexpr int MT = MT_, NB = NB_, MINB = MINB_;
     static constexpr bool BORDER = BORDER_;  // bordered prediction compiled in
     static constexpr int NWARP = MT / 16, NT = 32 * NWARP;
-    static constexpr int STAGES = 3;
+    static constexpr int STAGES = STAGES_;
     static constexpr int BS = NB + 4;   // Linv^T row stride: 2 BS == 8 (mod 32) words, conflict-free fragments
     static constexpr int LJS = NB + 1;  // row stride of the diagonal block in SMEM
     static constexpr int A_STAGE = MT * KC;
@@ -97,7 +97,14 @@ struct Geo {
     static_assert(MT == 16 * NWARP && (NB == 64 || NB == 32) && MT >= NB, "warp tile 16 x NB");
 };
 using GeoLarge = Geo<kMT, kNB, 2, false>;
-using GeoSmall = Geo<kMTSmall, kNBSmall, 4, true>;
+// (5 or 6 CTAs per SM with a 2-stage ring were measured slower: r02_ab_small_occupancy.json)
+#ifndef PGPCV_SMALL_MINB
+#define PGPCV_SMALL_MINB 4
+#endif
+#ifndef PGPCV_SMALL_STAGES
+#define PGPCV_SMALL_STAGES 3
+#endif
+using GeoSmall = Geo<kMTSmall, kNBSmall, PGPCV_SMALL_MINB, true, PGPCV_SMALL_STAGES>;
 
 // ---------------------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -224,10 +231,12 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
                  "r"((unsigned)(G::NB * KC * sizeof(double)))
                  : "memory");
 }
-// Refill protocol: 1 = the last warp to release a stage refills it (round 2); 0 = thread 0
-// issues chunk n + STAGES - 1 at the start of chunk n after waiting for every release.
+// Refill protocol: 0 = thread 0 issues chunk n + STAGES - 1 at the start of chunk n after
+// waiting for every release (round 1); 1 = the last warp to release a stage refills it, the
+// tile prologue issuing all STAGES chunks; 2 = as 1, but the prologue issues STAGES - 1 and
+// thread 0 the last one at the tile's first chunk.
 #ifndef PGPCV_LAST_REFILLS
-#define PGPCV_LAST_REFILLS 1
+#define PGPCV_LAST_REFILLS 0
 #endif
 // Column of the i-th operand chunk of a tile: ascending on even row tiles, descending on
 // odd ones (a boustrophedon over the k-chunks), so a tile starts with the B-panel chunks
@@ -242,7 +251,7 @@ __device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage
                                               uint64_t *empty, const double *L, int64_t ld, int r0,
                                               int j0, bool rev) {
     fence_proxy_async();
-    constexpr int PRO = PGPCV_LAST_REFILLS ? G::STAGES : G::STAGES - 1;  // chunks in flight at tile start
+    constexpr int PRO = PGPCV_LAST_REFILLS == 1 ? G::STAGES : G::STAGES - 1;  // chunks in flight at tile start
     for (int i = 0; i < min(PRO, nk); ++i)
         issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev));
     for (int i = PRO; i < min(PRO + PFD, nk); ++i)
@@ -448,15 +457,13 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
-#if !PGPCV_LAST_REFILLS
-                    if (tid == 0) {
+                    if (tid == 0 && (PGPCV_LAST_REFILLS != 1) && (PGPCV_LAST_REFILLS == 0 || kc == 0)) {
                         if (kc + STAGES - 1 < nk)
                             issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
                                            chunk_col(kc + STAGES - 1, nk, rt & 1));
                         if (kc + STAGES - 1 + PFD < nk)
                             prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + PFD, nk, rt & 1));
                     }
-#endif
                     PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
                     PH(4);
@@ -498,6 +505,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                                      : "=r"(old) : "r"(smem_u32(&rel[n % STAGES])) : "memory");
                         if (old == NWARP - 1) {
                             rel[n % STAGES] = 0;
+                            // (mode 2: chunk STAGES - 1 of a tile is issued by thread 0 at kc = 0,
+                            // so the tile prologue never waits for the previous tile's last chunk)
                             if (kc + STAGES < nk)
                                 issue_chunk<G>(n + STAGES, stage, full, empty, L, ld, r0, j0,
                                                chunk_col(kc + STAGES, nk, rt & 1));
