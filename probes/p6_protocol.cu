@@ -52,7 +52,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 // A group chunk: MT x 16 doubles (16 KB); B: NB x 16 (8 KB); a "unit" = one 16-column group
 constexpr int AG = MT * 16, BG = NB * 16, UNIT = AG + BG;
 
-template <int KC, int STAGES, int FENCE, int PROD, int SPLIT, int LAST = 0>
+template <int KC, int STAGES, int FENCE, int PROD, int SPLIT, int LAST = 0, int PF2 = 0, int WB = 0>
 __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const double *buf, size_t nunits, long chunks,
                                                                         double *out) {
     constexpr int G = KC / 16;  // column groups per stage
@@ -92,7 +92,14 @@ __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const dou
         }
     };
     auto pref = [&](long n) {
-        for (int gi = 0; gi < G; ++gi) prefetch_l2(src(n, gi), UNIT * 8);
+        for (int gi = 0; gi < G; ++gi) {
+            if (PF2) {  // A and B separately, as cv_kernel (its A and B chunks are apart)
+                prefetch_l2(src(n, gi), AG * 8);
+                prefetch_l2(src(n, gi) + AG, BG * 8);
+            } else {
+                prefetch_l2(src(n, gi), UNIT * 8);
+            }
+        }
     };
     if (PROD && warp == NWARP) {  // the producer warp
         if (lane == 0) {
@@ -121,6 +128,10 @@ __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const dou
         }
         const int s = n % STAGES;
         const unsigned par = (n / STAGES) & 1;
+        if (WB) {  // wait before the fragment loop, as cv_kernel
+            mbar_wait(&full[s], par);
+            __syncwarp();
+        }
 #pragma unroll
         for (int gi = 0; gi < G; ++gi) {
             const double *As = smem + s * STAGE + gi * UNIT;
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const dou
             const double *bp = As + AG + g * 16 + t;
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4) {
-                if (SPLIT ? (k4 == 0 || k4 == 2) : (gi == 0 && k4 == 0)) {
+                if (!WB && (SPLIT ? (k4 == 0 || k4 == 2) : (gi == 0 && k4 == 0))) {
                     mbar_wait(&full[SPLIT ? s * 2 + (k4 >> 1) : s], par);
                     __syncwarp();
                 }
@@ -173,15 +184,15 @@ struct Variant {
     void (*launch)(int, size_t, const double *, size_t, long, double *);
 };
 
-template <int KC, int ST, int F, int P, int S, int LA>
+template <int KC, int ST, int F, int P, int S, int LA, int PF2, int WB>
 void launch_v(int blocks, size_t smem, const double *buf, size_t nunits, long chunks, double *out) {
-    proto_kernel<KC, ST, F, P, S, LA><<<blocks, 32 * (NWARP + P), smem>>>(buf, nunits, chunks, out);
+    proto_kernel<KC, ST, F, P, S, LA, PF2, WB><<<blocks, 32 * (NWARP + P), smem>>>(buf, nunits, chunks, out);
 }
-template <int KC, int ST, int F, int P, int S, int LA = 0>
+template <int KC, int ST, int F, int P, int S, int LA = 0, int PF2 = 0, int WB = 0>
 Variant mk(const char *name) {
-    CK(cudaFuncSetAttribute(proto_kernel<KC, ST, F, P, S, LA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(proto_kernel<KC, ST, F, P, S, LA, PF2, WB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             ST * (KC / 16) * UNIT * 8));
-    return Variant{name, KC, ST, F, P, S, launch_v<KC, ST, F, P, S, LA>};
+    return Variant{name, KC, ST, F, P, S, launch_v<KC, ST, F, P, S, LA, PF2, WB>};
 }
 
 int main(int argc, char **argv) {
@@ -207,6 +218,9 @@ int main(int argc, char **argv) {
         mk<16, 3, 1, 0, 0, 1>("KC16 S3 fence, last releasing warp refills"),
         mk<16, 4, 1, 0, 0, 1>("KC16 S4 fence, last releasing warp refills"),
         mk<32, 2, 1, 0, 0, 1>("KC32 S2 fence, last releasing warp refills"),
+        mk<16, 3, 1, 0, 0, 0, 1, 0>("round1 + A/B prefetched separately"),
+        mk<16, 3, 1, 0, 0, 0, 0, 1>("round1 + wait before the fragment loop"),
+        mk<16, 3, 1, 0, 0, 0, 1, 1>("round1 + both (= cv_kernel / P5 structure)"),
     };
     const int nv = sizeof(vs) / sizeof(vs[0]);
     const int blocks = 2 * p.multiProcessorCount;
