@@ -241,6 +241,11 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 // Column of the i-th operand chunk of a tile: ascending on even row tiles, descending on
 // odd ones (a boustrophedon over the k-chunks), so a tile starts with the B-panel chunks
 // the previous tile of the same block column read last -- still in L2.
+// Consumer-side proxy fence before a stage is released (1; 0 = experiment: the release's
+// mbarrier arrive alone orders the warp's fragment reads before the refill).
+#ifndef PGPCV_LOOP_FENCE
+#define PGPCV_LOOP_FENCE 1
+#endif
 #ifndef PGPCV_SNAKE
 #define PGPCV_SNAKE 1
 #endif
@@ -353,12 +358,19 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
         // Per item: bordering costs m k^2 DMMA flops (3m/k of the factorization); it replaces
         // the back-substitution only while m <= k / 20 (c3, c4; c2's m/k ~ 0.06 measured
         // 1.3 % slower bordered).  border_pred 2 borders every item (tests).
-        const int nbt = (G::BORDER && (a.flags & kCvPredict) &&
-                         (a.border_pred == 2 || (a.border_pred == 1 && 20 * m <= k))) ? m : 0;
+        const int nbt = G::BORDER ? (int)border_rows(a.flags, a.border_pred, k, m) : 0;
         const int kb = k + np + nbt;                    // last bordered row
         const double *vxi = a.vx + voff, *vyi = a.vy + voff;
         const int64_t ld = factor_ld(kb);
         const int nblk = (k + NB - 1) / NB;
+        // This subset's covariance for this range, generated once per call (sigma_kernel),
+        // when the call reuses it (small kernel only); else nullptr: generate per item.
+        const double *sg = nullptr;
+        if (G::BORDER && a.sig) {
+            const int64_t so = a.sig_off[s];
+            if (so >= 0) sg = a.sig + (size_t)a.sig_range[c] * a.sig_stride + so;
+        }
+        const int64_t sld = sigma_ld(k, nbt);
         const int64_t oi = (int64_t)s * a.out_C + (a.out_C > 1 ? c : 0);  // output entry
         // slot scratch after the packed factor: alpha (k, when not in SMEM), then the
         // inverse of every diagonal block (nblk x 64 x 64, row-major) for the solves
@@ -417,14 +429,45 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                         const int r = rbase + i * 8 + g;
                         const int nl = j * 8 + 2 * t + e;
                         const int cc = j0 + nl;
-                        const double dx = rx[i] - cx[nl], dy = ry[i] - cy[nl];
-                        double v = -exp_neg(sqrt_nb(dx * dx + dy * dy) * ninv, etab);
+                        double v = -cov_exp(rx[i] - cx[nl], ry[i] - cy[nl], ninv, etab);
                         v = r == cc ? -(1.0 + lam) : v;                 // exp(0) + lambda
                         v = r == k ? -cv[nl] : v;                       // bordered y_T
                         v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
                         acc[i][j][e] = v;
                     };
-                    if (live) {
+                    if (G::BORDER && sg && live) {
+                        // the entries of Sigma_theta from the per-range block (16-B loads of
+                        // the (2t, 2t+1) column pairs), then the same diagonal / y / padding
+                        // rules as the generation: bit-identical to generating them here
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) {
+                            const int r = rbase + i * 8 + g;
+                            const bool rok = r < k || (r > k && r <= k + nbt);
+#pragma unroll
+                            for (int j = 0; j < NJ; ++j) {
+                                const int c0 = j0 + j * 8 + 2 * t;
+                                double2 w = make_double2(0.0, 0.0);
+                                if (rok && c0 < k) w = __ldg(reinterpret_cast<const double2 *>(sg + lidx(sld, r, c0)));
+                                acc[i][j][0] = w.x;
+                                acc[i][j][1] = w.y;
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+#pragma unroll
+                            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int r = rbase + i * 8 + g;
+                                    const int nl = j * 8 + 2 * t + e;
+                                    const int cc = j0 + nl;
+                                    double v = -acc[i][j][e];
+                                    v = r == cc ? -(1.0 + lam) : v;
+                                    v = r == k ? -cv[nl] : v;
+                                    v = (cc >= k || r > kb || r < cc) ? 0.0 : v;
+                                    acc[i][j][e] = v;
+                                }
+                    } else if (live) {
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -492,7 +535,9 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                     // ordered before the async-proxy bulk copy that will refill it (the
                     // mbarrier alone orders only within the generic proxy; without this
                     // fence stale/partial operands were observed at ~1e-3 of items).
+#if PGPCV_LOOP_FENCE
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
                     __syncwarp();
                     if (lane == 0) {
                         mbar_arrive(&empty[n % STAGES]);
@@ -960,8 +1005,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             const double px = __ldg(vx + v), py = __ldg(vy + v);
             double sum = 0.0;
             for (int j = lane; j < k; j += 32) {
-                const double dx = px - __ldg(tx + j), dy = py - __ldg(ty + j);
-                sum += exp_neg(sqrt_nb(dx * dx + dy * dy) * ninv, etab) * alpha[j];
+                sum += cov_exp(px - __ldg(tx + j), py - __ldg(ty + j), ninv, etab) * alpha[j];
             }
             sum = warp_sum(sum);
             if (a.yhat && lane == 0) a.yhat[voff + v] = sum;
@@ -978,6 +1022,57 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             a.fail[oi] = 0;
         }
         PH(11);
+    }
+}
+
+// K4s sigma_kernel: Sigma_theta(s) = exp(-D_s / theta) for every small subset s of the call
+// and every distinct range theta of its configurations (Eq.3).  The covariance
+// depends on a configuration only through the range; lambda = nugget / sigma2 moves only the
+// diagonal, so the (range, lambda) items of one subset read these entries instead of
+// each regenerating the k^2/2 distances and exponentials (BASELINE north_star: distances
+// reused across parameter configurations).  kSigmaSplit CTAs per (subset, range), CTA p taking
+// column groups p, p + kSigmaSplit, ... (the call's subsets fill the GPU even at c2's 100), writing the block
+// in the factor's packed, swizzled column-group layout with ld = sigma_ld(k, nbt): rows
+// 0..k-1 the training points, rows k+1..k+nbt the bordered targets' cross-covariance, row k
+// (y) and entries above the diagonal or past column k zero.  Writes are fully coalesced
+// (consecutive threads, consecutive doubles); HBM-write-bound at 8 B per entry.
+constexpr int kSigmaSplit = 8;
+__global__ void __launch_bounds__(256) sigma_kernel(const int32_t *subs, int32_t n_subs, const double *ranges,
+                                                    const int64_t *train_off, const int64_t *val_off,
+                                                    const double *tx, const double *ty, const double *vx,
+                                                    const double *vy, int32_t flags, int32_t border_pred,
+                                                    double *sig, const int64_t *sig_off, size_t sig_stride) {
+    __shared__ double etab[EXP_TAB];
+    if (threadIdx.x < EXP_TAB) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
+    __syncthreads();
+    const int part = blockIdx.x % kSigmaSplit;
+    const int s = subs[(blockIdx.x / kSigmaSplit) % n_subs];
+    const int ri = blockIdx.x / kSigmaSplit / n_subs;
+    const int64_t toff = train_off[s], voff = val_off[s];
+    const int k = (int)(train_off[s + 1] - toff);
+    const int m = (int)(val_off[s + 1] - voff);
+    const int nbt = (int)border_rows(flags, border_pred, k, m);
+    const int64_t ld = sigma_ld(k, nbt);
+    const double ninv = -1.0 / ranges[ri];  // the kernel's own division (bit-identical)
+    double *out = sig + (size_t)ri * sig_stride + sig_off[s];
+    const double *px = tx + toff, *py = ty + toff, *qx = vx + voff, *qy = vy + voff;
+    const int groups = (k + KC - 1) / KC;
+    for (int q = part; q < groups; q += kSigmaSplit) {
+        const int64_t n = (ld - 16 * q) * KC;
+        double *blk = out + (size_t)(gbase(ld, q) + 16 * q) * KC;
+        for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) {
+            const int r = 16 * q + (int)(idx >> 4);
+            const int c = 16 * q + ((int)(idx & 15) ^ ((r & 3) << 2));
+            double v = 0.0;
+            if (c < k) {
+                if (r < k && r >= c)
+                    v = cov_exp(__ldg(px + r) - __ldg(px + c), __ldg(py + r) - __ldg(py + c), ninv, etab);
+                else if (r > k && r <= k + nbt)
+                    v = cov_exp(__ldg(qx + (r - k - 1)) - __ldg(px + c), __ldg(qy + (r - k - 1)) - __ldg(py + c),
+                                ninv, etab);
+            }
+            blk[idx] = v;
+        }
     }
 }
 
@@ -1169,6 +1264,22 @@ cudaError_t launch_expand(int64_t N, int32_t C, int32_t U, const int32_t *umap, 
     const int grid = (int)std::min<int64_t>((N * C + 255) / 256, 148 * 8);
     expand_kernel<<<grid, 256, 0, st>>>(N, C, U, umap, own, train_off, sigma2, u_loss, u_fail, u_logdet, u_zz, loss,
                                         fail, nll);
+    return cudaGetLastError();
+}
+
+int64_t sigma_doubles(int64_t k, int64_t nbt) {
+    const int64_t groups = (k + KC - 1) / KC;
+    return groups > 0 ? factor_doubles(sigma_ld(k, nbt), groups) : 0;
+}
+
+cudaError_t launch_sigma(const int32_t *subs, int32_t n_subs, const double *ranges, int32_t n_ranges,
+                         const int64_t *train_off, const int64_t *val_off, const double *tx, const double *ty,
+                         const double *vx, const double *vy, int32_t flags, int32_t border_pred, double *sig,
+                         const int64_t *sig_off, size_t sig_stride, cudaStream_t st) {
+    if ((int64_t)n_subs * n_ranges == 0) return cudaSuccess;
+    sigma_kernel<<<(unsigned)((int64_t)n_subs * n_ranges * kSigmaSplit), 256, 0, st>>>(subs, n_subs, ranges, train_off, val_off, tx,
+                                                                         ty, vx, vy, flags, border_pred, sig, sig_off,
+                                                                         sig_stride);
     return cudaGetLastError();
 }
 

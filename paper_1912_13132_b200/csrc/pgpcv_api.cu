@@ -18,11 +18,21 @@
 #include <nccl.h>
 
 #include "../../include/pgpcv.h"
+#include <nvtx3/nvToolsExt.h>
 #include "pgpcv_internal.h"
 
 using namespace pgpcv;
 
 namespace {
+
+// NVTX range over a scope (an nsys / ncu timeline shows each API call and the phases of an
+// evaluation by name; header-only NVTX v3, a no-op unless a tool is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ------------------------------------------------------------------ device buffers
 template <typename T>
@@ -207,6 +217,16 @@ struct pgpcv_ctx {
 
     // cv_loss buffers
     DevBuf<double> work;
+    // per-range covariance reuse (small kernel): the blocks, per-subset offsets, the call's
+    // small subsets, distinct ranges and each unique config's range index
+    DevBuf<double> sig, sig_ranges;
+    DevBuf<int64_t> sig_off;
+    DevBuf<int32_t> sig_subs, sig_range;
+    uint64_t partition_gen = 0;        // bumped by every partition (invalidates the cached layout)
+    std::vector<int32_t> h_sig_subs;   // the device copies' host image (layout cache)
+    std::vector<int64_t> h_sig_off;
+    uint64_t sig_gen = ~0ull;          // partition_gen of the uploaded layout
+    size_t sig_layout_stride = 0;
     DevBuf<double> params;
     DevBuf<int2> items;
     DevBuf<unsigned long long> counter;
@@ -233,6 +253,9 @@ struct pgpcv_ctx {
     DevBuf<int32_t> sel_best, sel_wins;
     int blocks_per_sm[2] = {0, 0};  // resident CTAs per SM of the large / small kernel
     int64_t small_k = 2048;         // subsets with k <= small_k run on the small kernel (PGPCV_SMALL_K)
+    int sigma_reuse = 1;            // small kernel: per-range covariance blocks (PGPCV_SIGMA_REUSE: 0 never,
+                                    // 1 where a subset has >= 1.5 items per range in the call, 2 always)
+    double sigma_budget = 0.5;      // at most this fraction of the free device memory for the blocks
     int border_pred = 1;            // small kernel: bordered prediction where m <= k/20 (PGPCV_BORDER_PRED:
                                     // 0 never, 2 always)
     cudaStream_t aux_stream = nullptr;  // the small kernel's stream when both kernels run
@@ -465,6 +488,7 @@ int partition_impl(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, 
     info.n_test = sum_g;
     info.max_test = max_g;
     ctx->has_partition = true;
+    ++ctx->partition_gen;
     ctx->cv_done = false;
     ctx->sel_C = 0;
     ctx->owned.assign(N, 1);  // each evaluation assigns its own work (assign_owned)
@@ -547,6 +571,7 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
     if (const char *env = getenv("PGPCV_SMALL_K")) ctx->small_k = atoll(env);
     if (const char *env = getenv("PGPCV_BORDER_PRED")) ctx->border_pred = atoi(env);
+    if (const char *env = getenv("PGPCV_SIGMA_REUSE")) ctx->sigma_reuse = atoi(env);
     *out = ctx;
     return PGPCV_OK;
 }
@@ -596,6 +621,7 @@ static int check_partition_args(pgpcv_ctx *ctx, int64_t n, const void *x, const 
 int pgpcv_partition(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, const double *value,
                     const uint8_t *role, pgpcv_rect domain, int32_t kx, int32_t ky, double delta,
                     pgpcv_partition_info *info_out) {
+    NvtxRange nvtx_("pgpcv_partition");
     if (!ctx) return PGPCV_EINVAL;
     int rc = check_partition_args(ctx, n, x, y, value, role, domain, kx, ky, delta);
     if (rc) return rc;
@@ -621,6 +647,7 @@ int pgpcv_partition(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y,
 int pgpcv_partition_device(pgpcv_ctx *ctx, int64_t n, const double *d_x, const double *d_y,
                            const double *d_value, const uint8_t *d_role, pgpcv_rect domain,
                            int32_t kx, int32_t ky, double delta, pgpcv_partition_info *info_out) {
+    NvtxRange nvtx_("pgpcv_partition_device");
     if (!ctx) return PGPCV_EINVAL;
     int rc = check_partition_args(ctx, n, d_x, d_y, d_value, d_role, domain, kx, ky, delta);
     if (rc) return rc;
@@ -645,6 +672,7 @@ static int bisect_spec(pgpcv_ctx *ctx, int32_t depth, double delta, int64_t shel
 int pgpcv_partition_bisect(pgpcv_ctx *ctx, int64_t n, const double *x, const double *y, const double *value,
                            const uint8_t *role, pgpcv_rect domain, int32_t depth, double delta, int64_t shell_cap,
                            uint64_t seed, pgpcv_partition_info *info_out) {
+    NvtxRange nvtx_("pgpcv_partition_bisect");
     if (!ctx) return PGPCV_EINVAL;
     int rc = check_partition_args(ctx, n, x, y, value, role, domain, 1, 1, delta);
     if (rc) return rc;
@@ -668,6 +696,7 @@ int pgpcv_partition_bisect(pgpcv_ctx *ctx, int64_t n, const double *x, const dou
 int pgpcv_partition_bisect_device(pgpcv_ctx *ctx, int64_t n, const double *d_x, const double *d_y,
                                   const double *d_value, const uint8_t *d_role, pgpcv_rect domain, int32_t depth,
                                   double delta, int64_t shell_cap, uint64_t seed, pgpcv_partition_info *info_out) {
+    NvtxRange nvtx_("pgpcv_partition_bisect_device");
     if (!ctx) return PGPCV_EINVAL;
     int rc = check_partition_args(ctx, n, d_x, d_y, d_value, d_role, domain, 1, 1, delta);
     if (rc) return rc;
@@ -714,6 +743,7 @@ int pgpcv_nccl_get_unique_id(void *out) {
 }
 
 int pgpcv_shard(pgpcv_ctx *ctx, int rank, int world, const void *nccl_unique_id) {
+    NvtxRange nvtx_("pgpcv_shard");
     if (!ctx) return PGPCV_EINVAL;
     if (world < 1 || rank < 0 || rank >= world)
         return ctx->fail_with(PGPCV_EINVAL, "need 0 <= rank < world");
@@ -793,6 +823,12 @@ struct CvLaunch {
     int slots = 0;
 };
 
+uint64_t dbits(double v) {
+    uint64_t u;
+    memcpy(&u, &v, sizeof u);
+    return u;
+}
+
 // One batched evaluation of `items` (subset, config) in LPT order (descending k): items
 // with k > small_k run on the large-subset kernel, the rest on the small-subset kernel
 // (cv_kernel.cu, Geo<128,64,2> / Geo<64,32,4>), the two launched on forked streams so the
@@ -800,6 +836,7 @@ struct CvLaunch {
 // gets one factor slot per resident CTA, sized for its largest subset.  Records the span
 // of the launches on ctx->ev[1..2].  Outputs are device arrays of stride out_C (CvArgs).
 int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
+    NvtxRange nvtx_("run_cv");
     cudaStream_t st = ctx->stream;
     auto kof = [&](const int2 &it) { return ctx->h_train_off[it.x + 1] - ctx->h_train_off[it.x]; };
     // LPT: descending k (stable, so ties keep ascending subset / config order)
@@ -873,6 +910,78 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         CK(cudaMemcpyAsync(ctx->items.p, L.items.data(), sizeof(int2) * n_items, cudaMemcpyHostToDevice, st),
            "copy items");
     CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long) * 2 * (1 + kMaxSms), st), "memset");
+    // Per-range covariance reuse for the small kernel (K4s): when the
+    // small items outnumber the (subset, range) blocks by half again (or always with
+    // PGPCV_SIGMA_REUSE=2), Sigma_theta of every small subset is generated once per range by
+    // sigma_kernel and read by the items.  The blocks live for this call only (nothing is
+    // cached across calls but their layout, a function of the partition); skipped when they
+    // would take more than sigma_budget of the free device memory.
+    bool use_sig = false;
+    int32_t n_sub_small = 0, n_ranges = 0;
+    size_t sig_stride = 0;
+    {
+        const Part &q = parts[1];
+        std::vector<int32_t> range_of(L.C);
+        std::vector<uint64_t> rkeys;
+        std::vector<double> rvals;
+        for (int c = 0; c < L.C; ++c) {
+            const uint64_t key = dbits(L.params[c].range);
+            int32_t r = (int32_t)(std::find(rkeys.begin(), rkeys.end(), key) - rkeys.begin());
+            if (r == (int32_t)rkeys.size()) {
+                rkeys.push_back(key);
+                rvals.push_back(L.params[c].range);
+            }
+            range_of[c] = r;
+        }
+        n_ranges = (int32_t)rkeys.size();
+        if (q.count && ctx->sigma_reuse > 0) {
+            std::vector<int32_t> subs;
+            std::vector<int64_t> off(ctx->N, -1);
+            size_t total_sig = 0;
+            for (int64_t i = q.first; i < q.first + q.count; ++i) {
+                const int s = L.items[i].x;
+                if (off[s] >= 0) continue;
+                const int64_t k = kof(L.items[i]), m = L.h_tgt_off[s + 1] - L.h_tgt_off[s];
+                off[s] = (int64_t)total_sig;
+                subs.push_back(s);
+                total_sig += (size_t)(sigma_doubles(k, border_rows(L.flags, q.border, k, m)) + 31) / 32 * 32;
+            }
+            // worth it when the items outnumber the blocks generated by half again (a block
+            // costs one generation; an item reading it saves one)
+            const bool want = ctx->sigma_reuse == 2 || 2 * q.count >= 3 * (int64_t)subs.size() * n_ranges;
+            const size_t need = total_sig * (size_t)n_ranges;
+            bool fits = want && need > 0 && need <= ctx->sig.cap;
+            if (want && need > 0 && !fits) {  // grow (the only place that asks for free memory)
+                size_t free_b = 0, tot_b = 0;
+                cudaMemGetInfo(&free_b, &tot_b);
+                fits = (double)need * sizeof(double) <= ctx->sigma_budget * (double)free_b &&
+                       ctx->sig.ensure(need) == cudaSuccess;
+            }
+            if (fits) {
+                const bool same = ctx->sig_gen == ctx->partition_gen && subs == ctx->h_sig_subs && off == ctx->h_sig_off;
+                if (!same) {
+                    CK(ctx->sig_off.ensure(ctx->N), "alloc");
+                    CK(ctx->sig_subs.ensure(subs.size()), "alloc");
+                    CK(cudaMemcpyAsync(ctx->sig_off.p, off.data(), sizeof(int64_t) * ctx->N, cudaMemcpyHostToDevice,
+                                       st), "copy");
+                    CK(cudaMemcpyAsync(ctx->sig_subs.p, subs.data(), sizeof(int32_t) * subs.size(),
+                                       cudaMemcpyHostToDevice, st), "copy");
+                    ctx->h_sig_subs.swap(subs);
+                    ctx->h_sig_off.swap(off);
+                    ctx->sig_gen = ctx->partition_gen;
+                }
+                CK(ctx->sig_ranges.ensure(n_ranges), "alloc");
+                CK(ctx->sig_range.ensure(L.C), "alloc");
+                CK(cudaMemcpyAsync(ctx->sig_ranges.p, rvals.data(), sizeof(double) * n_ranges, cudaMemcpyHostToDevice,
+                                   st), "copy");
+                CK(cudaMemcpyAsync(ctx->sig_range.p, range_of.data(), sizeof(int32_t) * L.C, cudaMemcpyHostToDevice,
+                                   st), "copy");
+                use_sig = true;
+                n_sub_small = (int32_t)ctx->h_sig_subs.size();
+                sig_stride = total_sig;
+            }
+        }
+    }
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     const bool both = parts[0].count && parts[1].count;
     if (both) {  // fork: the small kernel on the auxiliary stream
@@ -914,6 +1023,20 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         a.xmax = ctx->domain.xmax;
         a.ymax = ctx->domain.ymax;
         a.gls_out = L.gls_out;
+        a.sig = nullptr;
+        a.sig_off = nullptr;
+        a.sig_stride = 0;
+        a.sig_range = nullptr;
+        if (pi == 1 && use_sig) {
+            CK(launch_sigma(ctx->sig_subs.p, n_sub_small, ctx->sig_ranges.p, n_ranges, ctx->train_off.p, L.tgt_off,
+                            ctx->tx.p, ctx->ty.p, L.gx, L.gy, L.flags, q.border, ctx->sig.p, ctx->sig_off.p,
+                            sig_stride, ls), "sigma kernel launch");
+            ++L.launches;
+            a.sig = ctx->sig.p;
+            a.sig_off = ctx->sig_off.p;
+            a.sig_stride = sig_stride;
+            a.sig_range = ctx->sig_range.p;
+        }
         a.prof = nullptr;
 #ifdef PGPCV_PHASE_PROFILE
         DevBuf<unsigned long long> &prof = pi ? ctx->prof2 : ctx->prof;
@@ -1079,17 +1202,13 @@ int check_common(pgpcv_ctx *ctx) {
 
 int first_fail(int32_t a, int32_t b) { return a < 0 ? b : (b < 0 ? a : std::min(a, b)); }
 
-uint64_t dbits(double v) {
-    uint64_t u;
-    memcpy(&u, &v, sizeof u);
-    return u;
-}
 
 }  // namespace
 
 extern "C" {
 
 int pgpcv_evaluate(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, const pgpcv_outputs *out) {
+    NvtxRange nvtx_("pgpcv_evaluate");
     if (!ctx) return PGPCV_EINVAL;
     if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "evaluation needs a partition");
     if (!out) return ctx->fail_with(PGPCV_EINVAL, "NULL outputs");
@@ -1273,6 +1392,7 @@ int pgpcv_cv_loss(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, d
 
 int pgpcv_select(pgpcv_ctx *ctx, int32_t *best, double *rmspe, int32_t *local_best, double *local_rmspe,
                  int32_t *wins) {
+    NvtxRange nvtx_("pgpcv_select");
     if (!ctx) return PGPCV_EINVAL;
     if (ctx->sel_C <= 0)
         return ctx->fail_with(PGPCV_ESTATE, "pgpcv_select needs a preceding CV evaluation whose per-subset "
@@ -1301,6 +1421,7 @@ int pgpcv_select(pgpcv_ctx *ctx, int32_t *best, double *rmspe, int32_t *local_be
 
 int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, const int32_t *subset_config,
                   int32_t target_role, double *yhat, double *subset_sspe, double *sspe) {
+    NvtxRange nvtx_("pgpcv_predict");
     if (!ctx) return PGPCV_EINVAL;
     if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "pgpcv_predict needs a partition");
     int rc = check_params(ctx, params, n_params);
@@ -1385,6 +1506,7 @@ int pgpcv_predict(pgpcv_ctx *ctx, const pgpcv_param *params, int32_t n_params, c
 
 int pgpcv_gls(pgpcv_ctx *ctx, const double *X, int32_t p, pgpcv_param param, double *beta, double *xtmx,
               double *xtmy) {
+    NvtxRange nvtx_("pgpcv_gls");
     if (!ctx) return PGPCV_EINVAL;
     if (!ctx->has_partition) return ctx->fail_with(PGPCV_ESTATE, "pgpcv_gls needs a partition");
     if (p < 1 || p > kMaxCovariates) return ctx->fail_with(PGPCV_EINVAL, "need 1 <= p <= %d covariates", kMaxCovariates);

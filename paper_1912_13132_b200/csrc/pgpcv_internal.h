@@ -44,7 +44,30 @@ struct CvArgs {
     double *gls_out;            // [N * (p+1) * p]: A (p x p row-major) then b (p)
     unsigned long long *prof;   // [grid * 15] phase cycles (diagnostic build only) or nullptr
     unsigned long long *tl;     // [grid * 32768] GEMM/non-GEMM timeline (diagnostic) or nullptr
+    // Per-range covariance reuse (small kernel only; DESIGN.md section 6 "K4s"): Sigma_theta
+    // of each subset, generated once per call and range by sigma_kernel and read by every
+    // (range, lambda) item of that subset instead of regenerating the exp/sqrt.  nullptr:
+    // every item generates its own entries.
+    const double *sig;          // [n_ranges * sig_stride] packed factor layout, ld = sigma_ld(k, nbt)
+    const int64_t *sig_off;     // [N] offset (doubles) of subset s inside one range's block, -1: none
+    size_t sig_stride;          // doubles per range block
+    const int32_t *sig_range;   // [C] range index of config c
 };
+
+// Rows of the per-range covariance block of a subset: the k training rows, the y row
+// (never read from it) and the nbt bordered target rows.
+__host__ __device__ inline int64_t sigma_ld(int64_t k, int64_t nbt) { return ((k + nbt + 1 + 15) / 16) * 16; }
+// Targets bordered below y by the small kernel (bordered prediction, border_pred 1: where
+// 20 m <= k; 2: always), identical on the host and in both kernels.
+__host__ __device__ inline int64_t border_rows(int32_t flags, int32_t border_pred, int64_t k, int64_t m) {
+    return ((flags & 1) && (border_pred == 2 || (border_pred == 1 && 20 * m <= k))) ? m : 0;
+}
+cudaError_t launch_sigma(const int32_t *subs, int32_t n_subs, const double *ranges, int32_t n_ranges,
+                         const int64_t *train_off, const int64_t *val_off, const double *tx, const double *ty,
+                         const double *vx, const double *vy, int32_t flags, int32_t border_pred, double *sig,
+                         const int64_t *sig_off, size_t sig_stride, cudaStream_t st);
+// doubles of the packed per-range covariance block of a subset (column groups of 16 up to k)
+int64_t sigma_doubles(int64_t k, int64_t nbt);
 constexpr int32_t kCvPredict = 1;  // back-substitution, prediction, SSPE (Eq.3, Eq.4)
 constexpr int32_t kCvNll = 2;      // -2 log-likelihood from the same factor (Eq.2)
 constexpr int32_t kCvGls = 4;      // GLS normal-equation sums from the same factor (Eq. GLS)

@@ -26,7 +26,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
             ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
         else:
             ctx.partition_bisect(w.x, w.y, w.value, w.role, w.domain, w.depth, w.delta, w.shell_cap, w.cap_seed)
-        ctx.cv_loss(np.array([[1.0, 1.0, 0.1]]), want_subset_loss=False)
+        # P2_STEP=1: the bench's first step (5 grid configs: one range, several lambda --
+        # the per-range covariance reuse applies); default one config
+        params = w.params[0:5] if os.environ.get("P2_STEP") else np.array([[1.0, 1.0, 0.1]])
+        ctx.cv_loss(params, want_subset_loss=False)
         t = ctx.last_timing()
         print("TIMING", json.dumps(t), flush=True)
     sys.exit(0)

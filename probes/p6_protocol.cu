@@ -55,7 +55,11 @@ constexpr int AG = MT * 16, BG = NB * 16, UNIT = AG + BG;
 template <int KC, int STAGES, int FENCE, int PROD, int SPLIT, int LAST = 0, int PF2 = 0, int WB = 0>
 __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const double *buf, size_t nunits, long chunks,
                                                                         double *out) {
-    constexpr int G = KC / 16;  // column groups per stage
+    // KC = 8: 8-column groups (64-B rows; the swizzle moves rows 2-3 of every 4 to the other
+    // half-row, conflict-free fragment loads); KC >= 16: KC / 16 groups of 16 columns per stage
+    constexpr int W = KC < 16 ? KC : 16;
+    constexpr int AG = MT * W, BG = NB * W, UNIT = AG + BG;
+    constexpr int G = KC / W;  // column groups per stage
     constexpr int STAGE = G * UNIT;
     constexpr int NBAR = SPLIT ? 2 : 1;
     extern __shared__ __align__(128) double smem[];
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const dou
     __syncwarp();
     double acc[2][8][2];
     for (int i = 0; i < 2; ++i) for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int sw = (g & 3) << 2;
+    const int sw = W == 16 ? (g & 3) << 2 : ((g >> 1) & 1) << 2;
     for (long n = 0; n < chunks; ++n) {
         if (!PROD && !LAST && tid == 0) {
             if (n + STAGES - 1 < chunks) issue(n + STAGES - 1);
@@ -135,10 +139,10 @@ __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const dou
 #pragma unroll
         for (int gi = 0; gi < G; ++gi) {
             const double *As = smem + s * STAGE + gi * UNIT;
-            const double *ap = As + (warp * 16 + g) * 16 + t;
-            const double *bp = As + AG + g * 16 + t;
+            const double *ap = As + (warp * 16 + g) * W + t;
+            const double *bp = As + AG + g * W + t;
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
+            for (int k4 = 0; k4 < W / 4; ++k4) {
                 if (!WB && (SPLIT ? (k4 == 0 || k4 == 2) : (gi == 0 && k4 == 0))) {
                     mbar_wait(&full[SPLIT ? s * 2 + (k4 >> 1) : s], par);
                     __syncwarp();
@@ -146,9 +150,9 @@ __global__ void __launch_bounds__(32 * (NWARP + PROD), 2) proto_kernel(const dou
                 const int o = (k4 << 2) ^ sw;
                 double af[2], bf[8];
                 af[0] = ap[o];
-                af[1] = ap[8 * 16 + o];
+                af[1] = ap[8 * W + o];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * 16 + o];
+                for (int j = 0; j < 8; ++j) bf[j] = bp[j * 8 * W + o];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
 #pragma unroll
@@ -191,7 +195,7 @@ void launch_v(int blocks, size_t smem, const double *buf, size_t nunits, long ch
 template <int KC, int ST, int F, int P, int S, int LA = 0, int PF2 = 0, int WB = 0>
 Variant mk(const char *name) {
     CK(cudaFuncSetAttribute(proto_kernel<KC, ST, F, P, S, LA, PF2, WB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            ST * (KC / 16) * UNIT * 8));
+                            ST * KC * (MT + NB) * 8));
     return Variant{name, KC, ST, F, P, S, launch_v<KC, ST, F, P, S, LA, PF2, WB>};
 }
 
@@ -221,6 +225,11 @@ int main(int argc, char **argv) {
         mk<16, 3, 1, 0, 0, 0, 1, 0>("round1 + A/B prefetched separately"),
         mk<16, 3, 1, 0, 0, 0, 0, 1>("round1 + wait before the fragment loop"),
         mk<16, 3, 1, 0, 0, 0, 1, 1>("round1 + both (= cv_kernel / P5 structure)"),
+        mk<8, 6, 1, 0, 0, 0, 1, 1>("KC8 S6 fence (72 KB), thread-0 producer, cv_kernel structure"),
+        mk<8, 7, 1, 0, 0, 0, 1, 1>("KC8 S7 fence (84 KB), thread-0 producer, cv_kernel structure"),
+        mk<8, 6, 0, 0, 0, 0, 1, 1>("KC8 S6 no fence, thread-0 producer, cv_kernel structure"),
+        mk<16, 3, 0, 0, 0, 0, 1, 1>("KC16 S3 no fence, cv_kernel structure"),
+        mk<8, 6, 1, 0, 0, 1, 1, 1>("KC8 S6 fence, last releasing warp refills"),
     };
     const int nv = sizeof(vs) / sizeof(vs[0]);
     const int blocks = 2 * p.multiProcessorCount;
@@ -230,8 +239,8 @@ int main(int argc, char **argv) {
     for (int v = 0; v < nv; ++v) {
         if (which >= 0 && v != which) continue;
         const Variant &V = vs[v];
-        const size_t smem = (size_t)V.stages * (V.kc / 16) * UNIT * 8;
-        long chunks = 400 / (V.kc / 16);
+        const size_t smem = (size_t)V.stages * V.kc * (MT + NB) * 8;
+        long chunks = 400 * 16 / V.kc;
         V.launch(blocks, smem, buf, nunits, chunks, out);
         CK(cudaDeviceSynchronize());
         cudaEventRecord(a);
