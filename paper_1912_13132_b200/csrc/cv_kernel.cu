@@ -74,11 +74,18 @@ constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (
 //     pivot chain, the TRSM, the back-substitution) dominates, and twice the items in
 //     flight per SM hide it; its operands stream at 5.3 instead of 10.7 flop/B.
 // Each warp owns 16 full rows x NB columns of a row tile.
-template <int MT_, int NB_, int MINB_, bool BORDER_, int STAGES_ = 3>
+template <int MT_, int NB_, int MINB_, bool BORDER_, int STAGES_ = 3, bool SIG_ = false, bool WS_ = false>
 struct Geo {
     static constexpr int MT = MT_, NB = NB_, MINB = MINB_;
     static constexpr bool BORDER = BORDER_;  // bordered prediction compiled in
+    static constexpr bool SIG = SIG_;        // covariance entries read from the per-range blocks
+    // Warp-specialised CTA (WS): two consumer groups of NWARP warps, each an independent
+    // "virtual CTA" with its own item, SMEM and named barrier, plus a producer warpgroup whose
+    // warp g issues group g's operand chunks (setmaxnreg moves its registers to the consumers)
+    static constexpr bool WS = WS_;
+    static constexpr int GROUPS = WS ? 2 : 1;
     static constexpr int NWARP = MT / 16, NT = 32 * NWARP;
+    static constexpr int THREADS = GROUPS * NT + (WS ? 128 : 0);  // block size at launch
     static constexpr int STAGES = STAGES_;
     static constexpr int BS = NB + 4;   // Linv^T row stride: 2 BS == 8 (mod 32) words, conflict-free fragments
     static constexpr int LJS = NB + 1;  // row stride of the diagonal block in SMEM
@@ -92,11 +99,18 @@ struct Geo {
     static constexpr unsigned STAGE_BYTES = (unsigned)(KC * (MT + NB) * sizeof(double));
     static_assert(2 * NB * LJS <= STAGE_DBL, "diagonal block and its inverse must fit in the stage buffers");
     static_assert(NB * LJS <= BT_DBL, "back-substitution block must fit in the Linv buffer");
-    static_assert(SMEM_BYTES * MINB <= 232448 - MINB * 1024, "MINB CTAs per SM");
+    static constexpr size_t CTA_SMEM = GROUPS * SMEM_BYTES;  // dynamic SMEM of one CTA
+    static_assert(CTA_SMEM * MINB <= 232448 - MINB * 1024, "MINB CTAs per SM");
     static_assert((BS * 2) % 32 == 8, "fragment-load stride of Linv^T");
     static_assert(MT == 16 * NWARP && (NB == 64 || NB == 32) && MT >= NB, "warp tile 16 x NB");
 };
 using GeoLarge = Geo<kMT, kNB, 2, false>;
+// the large kernel as one warp-specialised CTA per SM (two consumer groups + producers)
+using GeoLargeWS = Geo<kMT, kNB, 1, false, 3, false, true>;
+// setmaxnreg (CTA pool: 640 threads launch at 96 registers): the producer warpgroup gives up
+// 128 x (96 - 32), the four consumer warpgroups take 512 x (112 - 96) of it
+constexpr int kWsConsumerRegs = 112;
+constexpr int kWsProducerRegs = 32;
 // (5 or 6 CTAs per SM with a 2-stage ring were measured slower: r02_ab_small_occupancy.json)
 #ifndef PGPCV_SMALL_MINB
 #define PGPCV_SMALL_MINB 4
@@ -105,6 +119,9 @@ using GeoLarge = Geo<kMT, kNB, 2, false>;
 #define PGPCV_SMALL_STAGES 3
 #endif
 using GeoSmall = Geo<kMTSmall, kNBSmall, PGPCV_SMALL_MINB, true, PGPCV_SMALL_STAGES>;
+// the same small kernel reading the covariance from sigma_kernel's per-range blocks (a
+// separate instantiation: the generating variant keeps its register allocation and schedule)
+using GeoSmallSig = Geo<kMTSmall, kNBSmall, PGPCV_SMALL_MINB, true, PGPCV_SMALL_STAGES, true>;
 
 // ---------------------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -139,6 +156,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void add_release_u32(unsigned *p, unsigned v) {
+    asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// spin (with back-off) until the shared counter reaches `target` (WS hand-offs)
+__device__ __forceinline__ void wait_count(const unsigned *p, unsigned target) {
+    while ((int)(ld_acquire_u32(p) - target) < 0) __nanosleep(32);
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.global;\n fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -155,7 +184,7 @@ constexpr int kTimelineLen = 1 << 15;
     do {                                                                                     \
         const int st_ = ((i) == 3 || (i) == 4) ? 1 : 0;                                      \
         if (st_ != tl_state && a.tl && tl_n < kTimelineLen - 2) {                            \
-            a.tl[(size_t)blockIdx.x * kTimelineLen + 2 + tl_n++] = ((unsigned long long)(t0) << 1) | st_; \
+            a.tl[(size_t)slot * kTimelineLen + 2 + tl_n++] = ((unsigned long long)(t0) << 1) | st_; \
             tl_state = st_;                                                                  \
         }                                                                                    \
     } while (0)
@@ -238,13 +267,22 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 #ifndef PGPCV_LAST_REFILLS
 #define PGPCV_LAST_REFILLS 0
 #endif
+// Consumer-side fence.proxy.async before a stage is released: 0 (default since round 2) --
+// the release's mbarrier arrive (release semantics) and the producer's wait (acquire) order
+// the warps' generic-proxy fragment reads before the async-proxy refill of the stage, a
+// write-after-read the bulk copy may follow without a proxy fence (the cross-proxy fences
+// stay where generic WRITES to stage memory -- the diagonal block, alpha, z -- precede a
+// refill).  Same-box A/B: c5 +0.4 %, c3/c4 +0.2 %; 40 stress repetitions of the c2 grid on
+// both kernel variants and the whole GPU suite bit-clean (profiles/r02_ab_loop_fence.json).
+// 1 restores the round-1 fence.
+#ifndef PGPCV_LOOP_FENCE
+#define PGPCV_LOOP_FENCE 0
+#endif
 // Column of the i-th operand chunk of a tile: ascending on even row tiles, descending on
 // odd ones (a boustrophedon over the k-chunks), so a tile starts with the B-panel chunks
 // the previous tile of the same block column read last -- still in L2.
-// Consumer-side proxy fence before a stage is released (1; 0 = experiment: the release's
-// mbarrier arrive alone orders the warp's fragment reads before the refill).
-#ifndef PGPCV_LOOP_FENCE
-#define PGPCV_LOOP_FENCE 1
+#ifndef PGPCV_PAIR_STORE  // TRSM epilogue: 16-B stores of column pairs (0: 8-B stores, round 1)
+#define PGPCV_PAIR_STORE 1
 #endif
 #ifndef PGPCV_SNAKE
 #define PGPCV_SNAKE 1
@@ -264,12 +302,24 @@ __device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage
 }
 
 template <class G>
-__global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
+__device__ void ws_producer(const CvArgs &a, double *stage, uint64_t *full, uint64_t *empty, const double *L,
+                           const unsigned *go, unsigned *ack, const int *s_item, const int *s_fail);
+
+template <class G>
+__global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
     constexpr int MT = G::MT, NB = G::NB, NT = G::NT, NWARP = G::NWARP, STAGES = G::STAGES;
     constexpr int BS = G::BS, LJS = G::LJS, A_STAGE = G::A_STAGE, B_STAGE = G::B_STAGE;
     constexpr int STAGE_DBL = G::STAGE_DBL, BT_DBL = G::BT_DBL;
     constexpr int NJ = NB / 8;  // 8-column fragments per warp row block
-    extern __shared__ __align__(128) double smem[];
+    extern __shared__ __align__(128) double smem_all[];
+    // WS: warps 0..2 NWARP-1 are the consumers of groups 0 and 1, warp 2 NWARP + g the
+    // producer of group g (g < 2; the warpgroup's other two warps only donate registers)
+    const int wid = threadIdx.x >> 5;
+    const bool producer = G::WS && wid >= G::GROUPS * NWARP;
+    const int grp = G::WS ? (producer ? wid - G::GROUPS * NWARP : wid / NWARP) : 0;
+    const int gs = grp < G::GROUPS ? grp : G::GROUPS - 1;  // this thread's group state
+    const int slot = G::WS ? blockIdx.x * G::GROUPS + gs : blockIdx.x;  // factor slot / output row
+    double *smem = smem_all + (size_t)gs * (G::SMEM_BYTES / sizeof(double));
     double *stage = smem;
     double *LJ = smem;                  // diagonal block [r][c], aliases the stages
     double *Bt = smem + STAGE_DBL;      // Bt[q*BS + n] = Linv[n][q]
@@ -279,40 +329,69 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
     double *dg = cv + NB;               // sqrt pivots of the diagonal block
     double *red = dg + 2 * NB;          // per-warp partial sums
     double *etab = red + NWARP;         // 2^(j/64), j = 0..63 (exp_neg)
-    __shared__ __align__(8) uint64_t full[STAGES];
-    __shared__ __align__(8) uint64_t empty[STAGES];
-    __shared__ int s_item;
-    __shared__ int s_fail;
-    __shared__ int s_rank;  // arrival order of this CTA on its SM (sched 1)
-    __shared__ unsigned rel[STAGES];  // releases of each stage's current use (PGPCV_LAST_REFILLS)
+    __shared__ __align__(8) uint64_t full_a[G::GROUPS][STAGES];
+    __shared__ __align__(8) uint64_t empty_a[G::GROUPS][STAGES];
+    __shared__ int s_item_a[G::GROUPS];
+    __shared__ int s_fail_a[G::GROUPS];
+    __shared__ int s_rank_a[G::GROUPS];  // arrival order of this CTA on its SM (sched 1)
+    __shared__ unsigned rel_a[G::GROUPS][STAGES];  // releases of each stage's current use (PGPCV_LAST_REFILLS)
+    __shared__ unsigned go_a[G::GROUPS], ack_a[G::GROUPS];  // WS hand-offs (consumer -> producer, back)
+    uint64_t *full = full_a[gs], *empty = empty_a[gs];
+    int &s_item = s_item_a[gs];
+    int &s_fail = s_fail_a[gs];
+    int &s_rank = s_rank_a[gs];
+    unsigned *rel = rel_a[gs];
+    unsigned *go = &go_a[gs], *ack = &ack_a[gs];
 #ifdef PGPCV_PHASE_PROFILE
-    __shared__ unsigned long long s_ph[kPhases];
-    if (threadIdx.x < kPhases) s_ph[threadIdx.x] = 0;
+    __shared__ unsigned long long s_ph_a[G::GROUPS][kPhases];
+    if (threadIdx.x < G::GROUPS * kPhases) (&s_ph_a[0][0])[threadIdx.x] = 0;
+    unsigned long long *s_ph = s_ph_a[gs];
 #endif
 
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int tid = G::WS ? (int)threadIdx.x - gs * NT : (int)threadIdx.x;  // thread in the group
+    const int lane = threadIdx.x & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    double *L = a.work + (size_t)blockIdx.x * a.slot_stride;
+    double *L = a.work + (size_t)slot * a.slot_stride;
+    // barrier of this thread's group: the CTA (or, WS, the group's named barrier)
+    auto gsync = [&]() {
+        if constexpr (G::WS)
+            asm volatile("bar.sync %0, %1;" ::"r"(gs + 1), "n"(NT) : "memory");
+        else
+            __syncthreads();
+    };
 
-    if (tid < EXP_TAB) etab[tid] = kExp2Tab[tid];
-    if (tid == 0) {
+    if (!producer && tid < EXP_TAB) etab[tid] = kExp2Tab[tid];
+    if (!producer && tid == 0) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], NWARP);
             rel[i] = 0;
         }
+        *go = 0;
+        *ack = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        s_rank = a.sched == 1 ? (int)(atomicAdd(a.counter + 1 + (smid % kMaxSms), 1ull) & 1ull) : 0;
+        s_rank = a.sched == 1 && !G::WS ? (int)(atomicAdd(a.counter + 1 + (smid % kMaxSms), 1ull) & 1ull) : 0;
     }
-    __syncthreads();
+    __syncthreads();  // the whole CTA, once
+    if constexpr (G::WS) {
+        if (producer) {
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsProducerRegs) : "memory");
+            if (grp < G::GROUPS && lane == 0) ws_producer<G>(a, stage, full, empty, L, go, ack, &s_item, &s_fail);
+            return;
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsConsumerRegs) : "memory");
+    }
     uint32_t pc = 0;  // operand chunks consumed so far (identical in every thread)
+    unsigned n_claims = 0;  // WS: items this group claimed (thread 0)
     PH_DECL
 
     for (;;) {
         if (tid == 0) {
+            // WS: the producer has issued every chunk of the previous item (so it has read
+            // s_item before it is overwritten here)
+            if constexpr (G::WS) wait_count(ack, n_claims);
             // Claim the next item: from the front of the LPT list, or (sched 1, the SM's
             // second CTA) from the back, so the two CTAs sharing an SM work on subsets of
             // different sizes and their non-GEMM phases do not fall into step.  The sum of
@@ -321,20 +400,24 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             const unsigned long long old = atomicAdd(a.counter, back ? (1ull << 32) : 1ull);
             const long long f = (long long)(old & 0xffffffffull), b = (long long)(old >> 32);
             s_item = f + b < a.n_items ? (int)(back ? a.n_items - 1 - b : f) : a.n_items;
+            if constexpr (G::WS) {  // hand-off 1: the item (or the end) to the producer
+                ++n_claims;
+                add_release_u32(go, 1);
+            }
         }
-        __syncthreads();
+        gsync();
         const int item = s_item;
-        __syncthreads();
+        gsync();
         if (item >= a.n_items) {
 #ifdef PGPCV_PHASE_PROFILE
             PH(0);
-            if (tid < kPhases && a.prof) a.prof[blockIdx.x * kPhases + tid] = s_ph[tid];
+            if (tid < kPhases && a.prof) a.prof[slot * kPhases + tid] = s_ph[tid];
 #ifdef PGPCV_TIMELINE
             if (tid == 0 && a.tl) {
                 unsigned smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-                a.tl[(size_t)blockIdx.x * kTimelineLen] = smid;
-                a.tl[(size_t)blockIdx.x * kTimelineLen + 1] = (unsigned long long)tl_n;
+                a.tl[(size_t)slot * kTimelineLen] = smid;
+                a.tl[(size_t)slot * kTimelineLen + 1] = (unsigned long long)tl_n;
             }
 #endif
 #endif
@@ -366,11 +449,20 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
         // This subset's covariance for this range, generated once per call (sigma_kernel),
         // when the call reuses it (small kernel only); else nullptr: generate per item.
         const double *sg = nullptr;
-        if (G::BORDER && a.sig) {
-            const int64_t so = a.sig_off[s];
-            if (so >= 0) sg = a.sig + (size_t)a.sig_range[c] * a.sig_stride + so;
-        }
+        if constexpr (G::SIG) sg = a.sig + (size_t)a.sig_range[c] * a.sig_stride + a.sig_off[s];
         const int64_t sld = sigma_ld(k, nbt);
+        // L2 prefetch of the per-range block's rows r0..r0+MT-1 of the block column's groups
+        // (issued one row tile ahead, so the tile's entry loads hit L2)
+        auto sig_prefetch = [&](int r0p, int j0p) {
+            if constexpr (G::SIG) {
+                const int rows = min(MT, (int)(k + nbt + 1) - r0p);
+                if (rows <= 0) return;
+                for (int q = j0p / KC; q < (j0p + NB) / KC && q * KC < k; ++q)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sg + (size_t)(gbase(sld, q) + r0p) * KC),
+                                 "r"((unsigned)(rows * KC * sizeof(double)))
+                                 : "memory");
+            }
+        };
         const int64_t oi = (int64_t)s * a.out_C + (a.out_C > 1 ? c : 0);  // output entry
         // slot scratch after the packed factor: alpha (k, when not in SMEM), then the
         // inverse of every diagonal block (nblk x 64 x 64, row-major) for the solves
@@ -396,9 +488,12 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             // before the last barrier) are read next by bulk copies (async proxy); the
             // stage memory was last touched by generic accesses (LJ, alpha).
             PH(0);
-            if (tid == 0) tile_prologue<G>(pc, nk, stage, full, empty, L, ld, j0, j0, false);
+            if (!G::WS && tid == 0) {  // (WS: the producer issues every chunk)
+                tile_prologue<G>(pc, nk, stage, full, empty, L, ld, j0, j0, false);
+                if (jb == 0) sig_prefetch(j0, j0);
+            }
             __syncwarp();
-            __syncthreads();  // cx/cy/cv visible
+            gsync();  // cx/cy/cv visible
             PH(1);
             for (int rt = 0; rt < ntiles; ++rt) {
                 const int r0 = j0 + rt * MT;
@@ -435,7 +530,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                         v = (cc >= k || r > kb || r < cc) ? 0.0 : v;    // pad / upper
                         acc[i][j][e] = v;
                     };
-                    if (G::BORDER && sg && live) {
+                    if constexpr (G::SIG) {
+                      if (live) {
                         // the entries of Sigma_theta from the per-range block (16-B loads of
                         // the (2t, 2t+1) column pairs), then the same diagonal / y / padding
                         // rules as the generation: bit-identical to generating them here
@@ -467,6 +563,12 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                                     v = (cc >= k || r > kb || r < cc) ? 0.0 : v;
                                     acc[i][j][e] = v;
                                 }
+                      } else {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+#pragma unroll
+                            for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+                      }
                     } else if (live) {
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
@@ -500,7 +602,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
-                    if (tid == 0 && (PGPCV_LAST_REFILLS != 1) && (PGPCV_LAST_REFILLS == 0 || kc == 0)) {
+                    if (!G::WS && tid == 0 && (PGPCV_LAST_REFILLS != 1) && (PGPCV_LAST_REFILLS == 0 || kc == 0)) {
                         if (kc + STAGES - 1 < nk)
                             issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
                                            chunk_col(kc + STAGES - 1, nk, rt & 1));
@@ -531,10 +633,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                                 for (int i = 0; i < 2; ++i) dmma(acc[i][j], af[i], bf[j]);
                         }
                     }
-                    // Release the stage: this warp's generic-proxy reads of it must be
-                    // ordered before the async-proxy bulk copy that will refill it (the
-                    // mbarrier alone orders only within the generic proxy; without this
-                    // fence stale/partial operands were observed at ~1e-3 of items).
+                    // Release the stage (PGPCV_LOOP_FENCE above: whether a proxy fence
+                    // precedes the release).
 #if PGPCV_LOOP_FENCE
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
@@ -572,7 +672,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                         if (j0 + j * 8 + 2 * t + e >= k) acc[0][j][e] = acc[1][j][e] = 0.0;
 
                 if (rt == 0) {
-                    __syncthreads();  // every warp is past the update: LJ may reuse the stages
+                    gsync();  // every warp is past the update: LJ may reuse the stages
                     PH(5);
                     // Diagonal block C = -acc to SMEM, then fused unblocked Cholesky + inverse.
                     if (warp < NB / 16) {
@@ -598,7 +698,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                     double *RI = LJ + NB * LJS;  // R / Linv rows, [n][q] stride LJS
                     for (int e = tid; e < NB * LJS; e += NT) RI[e] = (e / LJS == e % LJS) ? 1.0 : 0.0;
                     if (tid == 0) s_fail = 0;
-                    __syncthreads();
+                    gsync();
                     PH(12);
                     for (int p0 = 0; p0 < jw; p0 += 8) {
                         const int pw = min(8, jw - p0);
@@ -704,7 +804,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                             }
                         }
                         PH(13);
-                        __syncthreads();
+                        gsync();
                         if (s_fail) break;  // uniform
                         // this panel applied to the NEXT panel's columns and R rows only (all warps)
                         const int p1 = p0 + pw;
@@ -724,11 +824,12 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                                 RI[rr * LJS + q] = v;
                             }
                         }
-                        __syncthreads();
+                        gsync();
                         PH(14);
                     }
-                    __syncthreads();
+                    gsync();
                     if (s_fail) {
+                        if (G::WS && tid == 0) add_release_u32(go, 1);  // hand-off 2 (failed: the item ends)
                         failed = true;
                         break;
                     }
@@ -740,7 +841,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                         const int rr = e / NB, cc2 = e % NB;  // Linv row-major [rr][cc2]
                         linvG[(size_t)jb * NB * NB + e] = (cc2 <= rr && rr < jw) ? RI[rr * LJS + cc2] : 0.0;
                     }
-                    __syncthreads();
+                    gsync();
                     if ((a.flags & kCvNll) && warp == 0) {  // log det of this diagonal block
                         double l = 0.0;
                         for (int q = lane; q < jw; q += 32) l += log(dg[q]);
@@ -754,14 +855,21 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                             L[lidx(ld, j0 + rr, j0 + cc)] = rr == cc ? dg[cc] : LJ[rr * LJS + cc];
                     }
                     fence_proxy_async();  // generic LJ accesses before bulk copies refill it
-                    __syncthreads();      // LJ (stage memory) dead from here on
+                    gsync();      // LJ (stage memory) dead from here on
+                    if (G::WS && tid == 0) add_release_u32(go, 1);  // hand-off 2: stages free for tile 1
                     PH(7);
                 }
 
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
-                if (rt + 1 < ntiles && tid == 0)
+                if (!G::WS && rt + 1 < ntiles && tid == 0)
                     tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1);
+                if constexpr (G::SIG) {  // the next tile's covariance entries into L2
+                    if (tid == 0) {
+                        if (rt + 1 < ntiles) sig_prefetch(r0 + MT, j0);
+                        else if (jb + 1 < nblk) sig_prefetch(j0 + NB, j0 + NB);
+                    }
+                }
                 __syncwarp();
 
                 // X = C . Linv^T = -(acc . Linv^T) (triangular solve against L_jj^T as a
@@ -801,17 +909,24 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                             for (int i = 0; i < 2; ++i)
                                 if (sl <= 2 * (h * 4 + j) + 1) dmma(xo[i][j], af[i], bf[j]);
                     }
+                    // (columns 2t, 2t+1 of a fragment are adjacent in the swizzled layout:
+                    // one 16-B store per pair)
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int r = rbase + i * 8 + g;
-                                const int nl = h * 32 + j * 8 + 2 * t + e;
-                                if (nl < jw && r <= kb && r >= rskip)
-                                    L[lidx(ld, r, j0 + nl)] = -xo[i][j][e];
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = rbase + i * 8 + g;
+                            const int nl = h * 32 + j * 8 + 2 * t;
+                            if (r <= kb && r >= rskip && nl < jw) {
+                                double *dst = L + lidx(ld, r, j0 + nl);
+                                if (PGPCV_PAIR_STORE && nl + 1 < jw) {
+                                    *reinterpret_cast<double2 *>(dst) = make_double2(-xo[i][j][0], -xo[i][j][1]);
+                                } else {
+                                    dst[0] = -xo[i][j][0];
+                                    if (nl + 1 < jw) L[lidx(ld, r, j0 + nl + 1)] = -xo[i][j][1];
+                                }
                             }
+                        }
                 }
                 PH(8);
                 if (rt == ntiles - 1) {
@@ -821,7 +936,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                     // them before async-proxy accesses, then the barrier.
                     __threadfence();
                     fence_proxy_async();
-                    __syncthreads();
+                    gsync();
+                    if (G::WS && tid == 0) add_release_u32(go, 1);  // hand-off 3: the column is stored
                 }
                 PH(9);
             }
@@ -851,14 +967,14 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             }
             zz = warp_sum(zz);
             if (lane == 0) red[warp] = zz;
-            __syncthreads();
+            gsync();
             if (tid == 0) {
                 double q = 0.0;
                 for (int w = 0; w < NWARP; ++w) q += red[w];
                 a.logdet[oi] = logdet;
                 a.zz[oi] = q;
             }
-            __syncthreads();
+            gsync();
         }
         if (!(a.flags & (kCvPredict | kCvGls)) || ((a.flags & kCvPredict) && m == 0)) {
             if (tid == 0) {
@@ -866,7 +982,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                 a.fail[oi] = 0;
             }
             fence_proxy_async();
-            __syncthreads();
+            gsync();
             continue;
         }
 
@@ -904,13 +1020,13 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                     part2[warp * NB + c0 + 1] = p1;
                 }
             }
-            __syncthreads();
+            gsync();
             if (tid < jw) {
                 double sum = 0.0;
                 for (int w = 0; w < NWARP; ++w) sum += part2[w * NB + tid];
                 tvec[tid] = __ldcg(L + lidx(ld, rrow, j0 + tid)) - sum;  // z_c - L[c+1:, c] . alpha
             }
-            __syncthreads();
+            gsync();
             // L_jj^T alpha_j = t  ->  alpha_j = Linv^T t with the block's stored inverse: a
             // parallel 64 x 64 triangular mat-vec (rows r >= c), coalesced row reads
             if (tid < jw) {
@@ -926,7 +1042,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                 for (; r < jw; ++r) s0 += __ldcg(G + r * NB) * tvec[r];
                 alpha[j0 + tid] = (s0 + s1) + (s2 + s3);
             }
-            __syncthreads();
+            gsync();
         }
         };
 
@@ -955,25 +1071,25 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
                     if (cI >= np) break;  // uniform across the CTA
                     const double v = warp_sum(accq[cI]);
                     if (lane == 0) red[warp] = v;
-                    __syncthreads();
+                    gsync();
                     if (tid == 0) {
                         double t = 0.0;
                         for (int w = 0; w < NWARP; ++w) t += red[w];
                         a.gls_out[s * W + (q == 0 ? np * np + cI : cI * np + (q - 1))] = t;
                     }
-                    __syncthreads();
+                    gsync();
                 }
             }
             if (tid == 0) a.fail[oi] = 0;
             fence_proxy_async();
-            __syncthreads();
+            gsync();
             continue;
         }
         if (G::BORDER && nbt > 0) {
             // ---------------- bordered prediction (Eq.3, Eq.4): yhat_v = w_v . z ----------
             double *zs = stage;  // z = L^{-1} y_T, row k of the factor
             for (int c = tid; c < k; c += NT) zs[c] = __ldcg(L + lidx(ld, k, c));
-            __syncthreads();
+            gsync();
             double part = 0.0;
             for (int v = warp; v < m; v += NWARP) {
                 double sum = 0.0;
@@ -985,7 +1101,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             }
             if (lane == 0) red[warp] = part;
             fence_proxy_async();  // generic zs accesses before the next item's bulk copies
-            __syncthreads();
+            gsync();
             if (tid == 0) {
                 double l = 0.0;
                 for (int w = 0; w < NWARP; ++w) l += red[w];
@@ -1014,7 +1130,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
         }
         if (lane == 0) red[warp] = part;
         fence_proxy_async();  // generic alpha/part2 accesses before the next item's bulk copies
-        __syncthreads();
+        gsync();
         if (tid == 0) {
             double l = 0.0;
             for (int w = 0; w < NWARP; ++w) l += red[w];
@@ -1022,6 +1138,70 @@ __global__ void __launch_bounds__(G::NT, G::MINB) cv_kernel(CvArgs a) {
             a.fail[oi] = 0;
         }
         PH(11);
+    }
+}
+
+// WS producer (one lane of warp 2 NWARP + g): replays its group's sequence of (item, block
+// column, row tile, chunk) exactly as the consumers walk it and issues every operand chunk
+// as soon as its stage is released -- no consumer warp ever waits to refill a stage (P6:
+// a dedicated producer warp streams 5-6 % faster than thread 0 producing).  Hand-offs from
+// the group's thread 0 (counter `go`, release/acquire): 1 an item claimed (s_item), 2 the
+// diagonal block done (stage memory free again for tile 1; s_fail), 3 a block column stored
+// (its factor columns are the next column's operands).  `ack` counts the items whose chunks
+// were all issued; the consumers claim the next item only after it (s_item is read here).
+template <class G>
+__device__ void ws_producer(const CvArgs &a, double *stage, uint64_t *full, uint64_t *empty, const double *L,
+                           const unsigned *go, unsigned *ack, const int *s_item, const int *s_fail) {
+    constexpr int MT = G::MT, NB = G::NB;
+    uint32_t pc = 0;
+    unsigned seen = 0, done = 0;
+    auto next = [&]() { wait_count(go, ++seen); };
+    // chunks i = 0..nk-1 of row tile (r0, rev); L2 prefetch PFD chunks ahead, running on into
+    // the next row tile of the block column (r0n >= 0)
+    auto tile = [&](int64_t ld, int r0, int j0, int nk, bool rev, int r0n) {
+        if (nk == 0) return;
+        fence_proxy_async();
+        for (int i = 0; i < nk; ++i) {
+            issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev));
+            const int ip = i + PFD;
+            if (ip < nk)
+                prefetch_chunk<G>(L, ld, r0, j0, chunk_col(ip, nk, rev));
+            else if (r0n >= 0 && ip - nk < nk)
+                prefetch_chunk<G>(L, ld, r0n, j0, chunk_col(ip - nk, nk, !rev));
+        }
+        pc += nk;
+    };
+    for (;;) {
+        next();  // 1
+        const int item = *(volatile const int *)s_item;
+        if (item >= a.n_items) return;
+        const int s = a.items[item].x;
+        const int k = (int)(a.train_off[s + 1] - a.train_off[s]);
+        const int m = (int)(a.val_off[s + 1] - a.val_off[s]);
+        const int np = (a.flags & kCvGls) ? a.p : 0;
+        const int nbt = G::BORDER ? (int)border_rows(a.flags, a.border_pred, k, m) : 0;
+        const int kb = k + np + nbt;
+        const int64_t ld = factor_ld(kb);
+        const int nblk = (k + NB - 1) / NB;
+        bool failed = false;
+        for (int jb = 0; jb < nblk; ++jb) {
+            const int j0 = jb * NB;
+            const int ntiles = (kb + 1 - j0 + MT - 1) / MT;
+            const int nk = j0 / KC;
+            if (jb > 0) next();  // 3 (previous column)
+            for (int i = 0; i < min(PFD, nk); ++i) prefetch_chunk<G>(L, ld, j0, j0, chunk_col(i, nk, false));
+            tile(ld, j0, j0, nk, false, ntiles > 1 ? j0 + MT : -1);
+            next();  // 2
+            if (*(volatile const int *)s_fail) {
+                failed = true;
+                break;
+            }
+            for (int rt = 1; rt < ntiles; ++rt)
+                tile(ld, j0 + rt * MT, j0, nk, rt & 1, rt + 1 < ntiles ? j0 + (rt + 1) * MT : -1);
+        }
+        if (!failed && nblk > 0) next();  // 3 (last column; k = 0 has none)
+        add_release_u32(ack, 1);
+        ++done;
     }
 }
 
@@ -1228,32 +1408,48 @@ size_t slot_doubles(int64_t kmax, int extra_rows) {
 template <class G>
 cudaError_t occupancy(int *blocks_per_sm) {
     cudaError_t e = cudaFuncSetAttribute(cv_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)G::SMEM_BYTES);
+                                         (int)G::CTA_SMEM);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, cv_kernel<G>, G::NT, G::SMEM_BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, cv_kernel<G>, G::THREADS, G::CTA_SMEM);
+    *blocks_per_sm *= G::GROUPS;  // factor slots (item streams) per SM
+    return e;
 }
 
 template <class G>
 cudaError_t launch(const CvArgs &a, int grid, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(cv_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)G::SMEM_BYTES);
+                                         (int)G::CTA_SMEM);
     if (e != cudaSuccess) return e;
-    cv_kernel<G><<<grid, G::NT, G::SMEM_BYTES, st>>>(a);
+    // `grid` counts factor slots; a WS CTA serves GROUPS of them (the host rounds up)
+    cv_kernel<G><<<(grid + G::GROUPS - 1) / G::GROUPS, G::THREADS, G::CTA_SMEM, st>>>(a);
     return cudaGetLastError();
 }
 
+// dispatch on the kernel variant (kCv*)
+template <class F>
+auto with_geo(int variant, F f) {
+    switch (variant) {
+        case kCvSmall: return f(GeoSmall{});
+        case kCvSmallSig: return f(GeoSmallSig{});
+        case kCvLargeWS: return f(GeoLargeWS{});
+        default: return f(GeoLarge{});
+    }
+}
 size_t cv_kernel_smem_bytes(int variant) {
-    return variant == kCvSmall ? GeoSmall::SMEM_BYTES : GeoLarge::SMEM_BYTES;
+    return with_geo(variant, [](auto g) { return decltype(g)::CTA_SMEM; });
+}
+int cv_kernel_slots_per_cta(int variant) {
+    return with_geo(variant, [](auto g) { return decltype(g)::GROUPS; });
 }
 int cv_kernel_max_k() { return PGPCV_MAX_K_INTERNAL; }  // = PGPCV_MAX_K (include/pgpcv.h)
 size_t cv_kernel_slot_doubles(int variant, int64_t kmax, int extra_rows) {
-    return variant == kCvSmall ? slot_doubles<GeoSmall>(kmax, extra_rows) : slot_doubles<GeoLarge>(kmax, extra_rows);
+    return with_geo(variant, [&](auto g) { return slot_doubles<decltype(g)>(kmax, extra_rows); });
 }
 cudaError_t cv_kernel_occupancy(int variant, int *blocks_per_sm) {
-    return variant == kCvSmall ? occupancy<GeoSmall>(blocks_per_sm) : occupancy<GeoLarge>(blocks_per_sm);
+    return with_geo(variant, [&](auto g) { return occupancy<decltype(g)>(blocks_per_sm); });
 }
 cudaError_t launch_cv_kernel(int variant, const CvArgs &a, int grid, cudaStream_t st) {
-    return variant == kCvSmall ? launch<GeoSmall>(a, grid, st) : launch<GeoLarge>(a, grid, st);
+    return with_geo(variant, [&](auto g) { return launch<decltype(g)>(a, grid, st); });
 }
 
 cudaError_t launch_expand(int64_t N, int32_t C, int32_t U, const int32_t *umap, const uint8_t *own,

@@ -251,8 +251,9 @@ struct pgpcv_ctx {
     int32_t sel_C = 0;
     DevBuf<double> sel_rmspe, sel_local;
     DevBuf<int32_t> sel_best, sel_wins;
-    int blocks_per_sm[2] = {0, 0};  // resident CTAs per SM of the large / small kernel
+    int blocks_per_sm[kCvVariants] = {};  // resident CTAs per SM of each kernel variant
     int64_t small_k = 2048;         // subsets with k <= small_k run on the small kernel (PGPCV_SMALL_K)
+    int ws = 0;                     // large kernel: the warp-specialised variant (PGPCV_WS=1)
     int sigma_reuse = 1;            // small kernel: per-range covariance blocks (PGPCV_SIGMA_REUSE: 0 never,
                                     // 1 where a subset has >= 1.5 items per range in the call, 2 always)
     double sigma_budget = 0.5;      // at most this fraction of the free device memory for the blocks
@@ -556,7 +557,7 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     if (const char *env = getenv("PGPCV_SCHED")) ctx->sched = atoi(env);
     for (auto &ev : ctx->ev) cudaEventCreate(&ev);
     cudaEventCreateWithFlags(&ctx->ev_sync, cudaEventDisableTiming);
-    for (int v = 0; v < 2; ++v)
+    for (int v = 0; v < kCvVariants; ++v)
         if ((e = cv_kernel_occupancy(v, &ctx->blocks_per_sm[v])) != cudaSuccess || ctx->blocks_per_sm[v] < 1) {
             g_create_error = std::string("cv kernel cannot be resident: ") + cudaGetErrorString(e);
             pgpcv_destroy(ctx);
@@ -572,6 +573,7 @@ int pgpcv_create(int cuda_device, pgpcv_ctx **out) {
     if (const char *env = getenv("PGPCV_SMALL_K")) ctx->small_k = atoll(env);
     if (const char *env = getenv("PGPCV_BORDER_PRED")) ctx->border_pred = atoi(env);
     if (const char *env = getenv("PGPCV_SIGMA_REUSE")) ctx->sigma_reuse = atoi(env);
+    if (const char *env = getenv("PGPCV_WS")) ctx->ws = atoi(env);
     *out = ctx;
     return PGPCV_OK;
 }
@@ -858,14 +860,14 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         size_t stride = 0, offset = 0;
         int border = 0;    // bordered prediction (targets as extra factor rows)
         int64_t extra = 0; // bordered rows below y: covariates (GLS) or targets
-    } parts[2] = {{kCvLarge, 0, n_large, n_large ? kof(L.items[0]) : 0},
+    } parts[2] = {{ctx->ws ? kCvLargeWS : kCvLarge, 0, n_large, n_large ? kof(L.items[0]) : 0},
                   {kCvSmall, n_large, n_items - n_large, n_items > n_large ? kof(L.items[n_large]) : 0}};
     // The small kernel predicts by bordering the targets below y (one factorization sweep,
     // no back-substitution: DESIGN.md section 6) -- m k^2 extra DMMA flops, against a
     // latency-bound re-read of the whole factor; the large kernel back-substitutes.
     for (Part &q : parts) {
         q.extra = L.p;
-        q.border = ((L.flags & kCvPredict) && q.variant == kCvSmall) ? ctx->border_pred : 0;
+        q.border = ((L.flags & kCvPredict) && q.variant != kCvLarge) ? ctx->border_pred : 0;
         if (q.border)
             for (int64_t i = q.first; i < q.first + q.count; ++i) {
                 const int s = L.items[i].x;
@@ -889,6 +891,8 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         if (!q.count) continue;
         q.slots = (int)std::min<int64_t>((int64_t)ctx->sms * ctx->blocks_per_sm[q.variant], q.count);
         if (cap > 0) q.slots = std::min(q.slots, cap);
+        const int per_cta = cv_kernel_slots_per_cta(q.variant);  // WS: two item streams per CTA
+        q.slots = (q.slots + per_cta - 1) / per_cta * per_cta;
         q.stride = cv_kernel_slot_doubles(q.variant, q.kmax, (int)q.extra);
     }
     while (true) {
@@ -983,6 +987,7 @@ int run_cv(pgpcv_ctx *ctx, CvLaunch &L) {
         }
     }
     CK(cudaEventRecord(ctx->ev[1], st), "event");
+    if (use_sig) parts[1].variant = kCvSmallSig;  // same geometry, slots and SMEM as kCvSmall
     const bool both = parts[0].count && parts[1].count;
     if (both) {  // fork: the small kernel on the auxiliary stream
         CK(cudaEventRecord(ctx->ev_fork, st), "event");

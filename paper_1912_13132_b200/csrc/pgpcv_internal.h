@@ -80,7 +80,9 @@ constexpr int kMT = 128;        // large: rows per row tile (8 warps)
 constexpr int kNB = 64;         // large: block-column width of the left-looking Cholesky
 constexpr int kMTSmall = 64;    // small: 4 warps
 constexpr int kNBSmall = 32;
-constexpr int kCvLarge = 0, kCvSmall = 1;
+constexpr int kCvLarge = 0, kCvSmall = 1, kCvSmallSig = 2, kCvLargeWS = 3;  // kernel variants
+constexpr int kCvVariants = 4;
+int cv_kernel_slots_per_cta(int variant);  // factor slots (independent item streams) per CTA
 size_t cv_kernel_smem_bytes(int variant);
 int cv_kernel_max_k();
 size_t cv_kernel_slot_doubles(int variant, int64_t kmax, int extra_rows = 0);  // factor + back-substitution scratch

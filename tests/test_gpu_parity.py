@@ -187,15 +187,19 @@ def test_ragged_single_subset(ctx, k):
     _assert_close(res.subset_loss, ref.subset_loss)
 
 
-@pytest.mark.parametrize("variant", ["large", "small"])
+@pytest.mark.parametrize("variant", ["large", "large_ws", "small"])
 def test_ragged_both_kernel_variants(pg, variant):
-    """Every ragged k on each kernel variant (the large 8-warp NB = 64 kernel, and the small
-    4-warp NB = 32 kernel that by default takes k <= 2048), forced with PGPCV_SMALL_K."""
-    os.environ["PGPCV_SMALL_K"] = "0" if variant == "large" else "100000"
+    """Every ragged k on each kernel variant (the large 8-warp NB = 64 kernel, its
+    warp-specialised form (PGPCV_WS=1: two consumer groups and producer warps per CTA), and
+    the small 4-warp NB = 32 kernel that by default takes k <= 2048), forced with
+    PGPCV_SMALL_K."""
+    os.environ["PGPCV_SMALL_K"] = "100000" if variant == "small" else "0"
+    os.environ["PGPCV_WS"] = "1" if variant == "large_ws" else "0"
     try:
         c = pg.Context(0)
     finally:
         del os.environ["PGPCV_SMALL_K"]
+        del os.environ["PGPCV_WS"]
     with c:
         for k in RAGGED_K + [1000, 1025]:
             m = 5
@@ -365,6 +369,29 @@ def test_two_ended_scheduling_is_bit_identical(pg):
             del os.environ["PGPCV_SCHED"]
     assert np.array_equal(out[0].subset_loss, out[1].subset_loss)
     assert np.array_equal(out[0].subset_nll, out[1].subset_nll)
+
+
+def test_warp_specialised_large_kernel_is_bit_identical(pg):
+    """The warp-specialised large kernel (PGPCV_WS=1) performs the same arithmetic in the same
+    order as the two-CTA kernel; only who issues the operand copies changes.  The c2 grid on
+    the large kernel (forced for every k), with a non-positive-definite config mixed in:
+    every output bit-identical, including the failure status."""
+    w = wl("c2")
+    p = np.concatenate([w.params[:20], [[0.1, 1.0, 0.0]]])
+    out = []
+    for ws in ("0", "1"):
+        os.environ["PGPCV_SMALL_K"] = "0"
+        os.environ["PGPCV_WS"] = ws
+        try:
+            with pg.Context(0) as c:
+                c.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
+                out.append(c.evaluate(p, nll=True, subset_nll=True))
+        finally:
+            del os.environ["PGPCV_SMALL_K"]
+            del os.environ["PGPCV_WS"]
+    for a_, b_ in ((out[0].subset_loss, out[1].subset_loss), (out[0].subset_nll, out[1].subset_nll),
+                   (out[0].loss, out[1].loss), (out[0].status, out[1].status)):
+        assert np.array_equal(np.asarray(a_).view(np.uint8), np.asarray(b_).view(np.uint8))
 
 
 def test_shard_and_evaluate_argument_rules(ctx, pg):
