@@ -786,22 +786,23 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                             // C columns >= f1 and the R rows >= f1.  This panel's own columns
                             // and R rows got the previous panel in the last iteration's second
                             // phase, so the two updates touch disjoint entries.
-                            const int q0 = p0 - 8, f1 = p0 + pw, mt = jw - f1;
-                            for (int e = tid - 32; e < mt * mt; e += NT - 32) {
-                                const int rr = f1 + e / mt, cc = f1 + e % mt;
-                                if (cc > rr) continue;
-                                double v = LJ[rr * LJS + cc];
+                            // (a row per warp, columns across the lanes: no index division and
+                            // no idle upper-triangle iterations)
+                            const int q0 = p0 - 8, f1 = p0 + pw;
+                            for (int rr = f1 + warp - 1; rr < jw; rr += NWARP - 1)
+                                for (int cc = f1 + lane; cc <= rr; cc += 32) {
+                                    double v = LJ[rr * LJS + cc];
 #pragma unroll
-                                for (int i = 0; i < 8; ++i) v -= LJ[rr * LJS + q0 + i] * LJ[cc * LJS + q0 + i];
-                                LJ[rr * LJS + cc] = v;
-                            }
-                            for (int e = tid - 32; e < mt * p0; e += NT - 32) {
-                                const int rr = f1 + e / p0, q = e % p0;
-                                double v = RI[rr * LJS + q];
+                                    for (int i = 0; i < 8; ++i) v -= LJ[rr * LJS + q0 + i] * LJ[cc * LJS + q0 + i];
+                                    LJ[rr * LJS + cc] = v;
+                                }
+                            for (int rr = f1 + warp - 1; rr < jw; rr += NWARP - 1)
+                                for (int q = lane; q < p0; q += 32) {
+                                    double v = RI[rr * LJS + q];
 #pragma unroll
-                                for (int i = 0; i < 8; ++i) v -= LJ[rr * LJS + q0 + i] * RI[(q0 + i) * LJS + q];
-                                RI[rr * LJS + q] = v;
-                            }
+                                    for (int i = 0; i < 8; ++i) v -= LJ[rr * LJS + q0 + i] * RI[(q0 + i) * LJS + q];
+                                    RI[rr * LJS + q] = v;
+                                }
                         }
                         PH(13);
                         gsync();
@@ -810,15 +811,17 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                         const int p1 = p0 + pw;
                         if (p1 < jw) {
                             const int mt = jw - p1, pn = min(8, mt);
-                            for (int e = tid; e < mt * pn; e += NT) {  // C[rr][cc] -= L[rr][panel] . L[cc][panel]
-                                const int rr = p1 + e / pn, cc = p1 + e % pn;
-                                if (cc > rr) continue;
+                            // (fixed power-of-two strides instead of index divisions)
+                            for (int e = tid; e < mt * 8; e += NT) {  // C[rr][cc] -= L[rr][panel] . L[cc][panel]
+                                const int rr = p1 + (e >> 3), cc = p1 + (e & 7);
+                                if (cc - p1 >= pn || cc > rr) continue;
                                 double v = LJ[rr * LJS + cc];
                                 for (int i = 0; i < pw; ++i) v -= LJ[rr * LJS + p0 + i] * LJ[cc * LJS + p0 + i];
                                 LJ[rr * LJS + cc] = v;
                             }
-                            for (int e = tid; e < pn * p1; e += NT) {  // R[rr][q] -= L[rr][panel] . Linv[panel][q]
-                                const int rr = p1 + e / p1, q = e % p1;
+                            for (int e = tid; e < pn * NB; e += NT) {  // R[rr][q] -= L[rr][panel] . Linv[panel][q]
+                                const int rr = p1 + e / NB, q = e % NB;
+                                if (q >= p1) continue;
                                 double v = RI[rr * LJS + q];
                                 for (int i = 0; i < pw; ++i) v -= LJ[rr * LJS + p0 + i] * RI[(p0 + i) * LJS + q];
                                 RI[rr * LJS + q] = v;
@@ -835,11 +838,15 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                     }
                     // Linv^T for the TRSM-as-GEMM: Bt[q][n] = Linv[n][q] (zero outside the block);
                     // Linv itself is kept per block column for the back-substitution.
+                    // (items that predict by bordering and do not back-substitute -- no GLS --
+                    // never read the stored inverses)
+                    const bool keep_linv = !(G::BORDER && nbt > 0 && np == 0);
                     for (int e = tid; e < NB * NB; e += NT) {
                         const int q = e / NB, nn = e % NB;
                         Bt[q * BS + nn] = (q <= nn && nn < jw) ? RI[nn * LJS + q] : 0.0;
                         const int rr = e / NB, cc2 = e % NB;  // Linv row-major [rr][cc2]
-                        linvG[(size_t)jb * NB * NB + e] = (cc2 <= rr && rr < jw) ? RI[rr * LJS + cc2] : 0.0;
+                        if (keep_linv)
+                            linvG[(size_t)jb * NB * NB + e] = (cc2 <= rr && rr < jw) ? RI[rr * LJS + cc2] : 0.0;
                     }
                     gsync();
                     if ((a.flags & kCvNll) && warp == 0) {  // log det of this diagonal block
@@ -849,11 +856,9 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                     }
                     PH(6);
                     // L_jj -> the factor (lower triangle; the diagonal from the pivots)
-                    for (int e = tid; e < jw * jw; e += NT) {
-                        const int rr = e / jw, cc = e % jw;
-                        if (rr >= cc)
+                    for (int rr = warp; rr < jw; rr += NWARP)  // a row per warp
+                        for (int cc = lane; cc <= rr; cc += 32)
                             L[lidx(ld, j0 + rr, j0 + cc)] = rr == cc ? dg[cc] : LJ[rr * LJS + cc];
-                    }
                     fence_proxy_async();  // generic LJ accesses before bulk copies refill it
                     gsync();      // LJ (stage memory) dead from here on
                     if (G::WS && tid == 0) add_release_u32(go, 1);  // hand-off 2: stages free for tile 1
@@ -1011,8 +1016,10 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                         const double ar = alpha[r];
                         const double *row = L + (size_t)(gbase(ld, grp) + r) * KC;
                         const int sw = (r & 3) << 2;
-                        p0 += __ldcg(row + ((c0 & 15) ^ sw)) * ar;
-                        p1 += __ldcg(row + (((c0 + 1) & 15) ^ sw)) * ar;
+                        // columns c0, c0 + 1 are adjacent in the swizzled row: one 16-B load
+                        const double2 lv = __ldcg(reinterpret_cast<const double2 *>(row + ((c0 & 15) ^ sw)));
+                        p0 += lv.x * ar;
+                        p1 += lv.y * ar;
                     }
                 }
                 if (c0 < NB) {
