@@ -97,11 +97,12 @@ NcclApi &nccl() {
     static bool tried = false;
     if (tried) return api;
     tried = true;
-    void *h = nccl_already_loaded();
-    if (!h) {
-        const char *env = getenv("PGPCV_NCCL_LIB");
-        if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
-    }
+    // PGPCV_NCCL_LIB, when set, is an explicit choice and is bound first, privately
+    // (RTLD_LOCAL: it never interposes on an NCCL the process already holds); otherwise an
+    // already-loaded NCCL is reused, else libnccl.so.2 is loaded.
+    void *h = nullptr;
+    if (const char *env = getenv("PGPCV_NCCL_LIB")) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = nccl_already_loaded();
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
         api.why = std::string("cannot dlopen libnccl.so.2: ") + dlerror();

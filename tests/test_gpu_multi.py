@@ -31,9 +31,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, shim=None):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    if shim:  # loopback: every rank on cuda:0, the combine through the host-memory shim
+        os.environ["PGPCV_NCCL_LIB"] = shim
     import torch
     import torch.distributed as dist
 
@@ -43,7 +45,8 @@ def _worker(rank, world, port, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(rank)
+    dev = 0 if shim else rank
+    torch.cuda.set_device(dev)
     out = {"nccl_library": pg.nccl_library()}
 
     def uid():
@@ -54,7 +57,7 @@ def _worker(rank, world, port, out_dir):
     w = workloads.make("c2", device="cpu")
     params = w.params[[0, 7, 37, 52, 74]]
     X = np.stack([np.ones(w.n), w.x, w.y], 1)
-    with pg.Context(rank) as ctx:
+    with pg.Context(dev) as ctx:
         def part():
             ctx.partition(w.x, w.y, w.value, w.role, w.domain, w.kx, w.ky, w.delta)
         part()
@@ -106,13 +109,9 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs (one rank per GPU)")
-def test_two_rank_shard_nccl(tmp_path):
-    import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
-    outs = [np.load(tmp_path / f"r{r}.npy", allow_pickle=True)[0] for r in range(2)]
+def _check(outs, library):
     for r, o in enumerate(outs):
-        assert "nvidia/nccl" in o["nccl_library"], o["nccl_library"]  # torch's NCCL reused
+        assert library in o["nccl_library"], o["nccl_library"]
         assert o["gather_subset_loss_equal"] and o["gather_subset_nll_equal"] and o["gather_loss_equal"], o
         assert o["vector_rel_err"] <= 1e-12, o
         assert o["predict_equal"] and o["gls_equal"], o
@@ -121,3 +120,35 @@ def test_two_rank_shard_nccl(tmp_path):
     assert outs[0]["my_evals"] > 0 and outs[1]["my_evals"] > 0  # both ranks worked
     import paper_1912_13132_b200 as pg
     assert outs[0]["fault_code"] == pg.ENCCL and outs[1]["fault_code"] == pg.ENOMEM
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs (one rank per GPU)")
+def test_two_rank_shard_nccl(tmp_path):
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    _check([np.load(tmp_path / f"r{r}.npy", allow_pickle=True)[0] for r in range(2)],
+           "nvidia/nccl")  # torch's NCCL reused
+
+
+def _build_shim(out_dir):
+    import subprocess
+
+    from paper_1912_13132_b200._build import _nccl_include
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "nccl_loopback", "loopback_nccl.c")
+    lib = os.path.join(out_dir, "libloopback_nccl.so")
+    subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-I", _nccl_include(), "-I", "/usr/local/cuda/include",
+                           src, "-o", lib, "-ldl", "-lrt"])
+    return lib
+
+
+@pytest.mark.skipif(_ngpu() < 1, reason="needs a GPU")
+def test_two_rank_shard_loopback_one_gpu(tmp_path):
+    """The same two-rank checks on ONE GPU: both ranks on cuda:0 and the eight NCCL entry
+    points bound from tests/nccl_loopback (PGPCV_NCCL_LIB; a host shared-memory all-reduce,
+    test infrastructure only).  Everything the library does at world > 1 -- LPT ownership,
+    gather and vector combines, the status MIN all-reduce, the error-flag lockstep and
+    re-sharding after an agreed failure -- runs on the GPU; only the transport is a stand-in."""
+    import torch.multiprocessing as mp
+    shim = _build_shim(str(tmp_path))
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), shim), nprocs=2, join=True)
+    _check([np.load(tmp_path / f"r{r}.npy", allow_pickle=True)[0] for r in range(2)], "libloopback_nccl.so")
