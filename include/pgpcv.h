@@ -227,10 +227,12 @@ int pgpcv_partition_export(pgpcv_ctx *ctx, int64_t *train_off, int32_t *train_id
  * (ncclCommAbort) and returns ENCCL; the ctx then needs pgpcv_shard again. */
 int pgpcv_shard(pgpcv_ctx *ctx, int rank, int world, const void *nccl_unique_id);
 
-/* Which libnccl the library bound (it reuses an NCCL already loaded in the process, e.g.
- * torch's, so one process never holds two): "path (NCCL x.y.z)" into buf[len], or the
- * reason none could be loaded.  Needs no ctx.  Errors: EINVAL (NULL / len < 1), ENCCL
- * (no usable libnccl; buf holds the reason). */
+/* Which libnccl the library bound: the file named by the environment variable
+ * PGPCV_NCCL_LIB when set (bound first and privately, RTLD_LOCAL -- an explicit choice,
+ * e.g. the tests' host-memory stand-in), else an NCCL already loaded in the process (e.g.
+ * torch's, so one process never holds two), else libnccl.so.2.  Writes "path (NCCL x.y.z)"
+ * into buf[len], or the reason none could be loaded.  Needs no ctx.  Errors: EINVAL (NULL /
+ * len < 1), ENCCL (no usable libnccl; buf holds the reason). */
 int pgpcv_nccl_library(char *buf, int64_t len);
 
 /* Fill `out` (NCCL_UNIQUE_ID_BYTES bytes) with a fresh ncclUniqueId.  Needs no ctx.
