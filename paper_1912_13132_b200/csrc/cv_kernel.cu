@@ -606,6 +606,8 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                         if (kc + STAGES - 1 < nk)
                             issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
                                            chunk_col(kc + STAGES - 1, nk, rt & 1));
+                        // (running this L2 prefetch on into the next row tile's first chunks
+                        // measured slower: c3 -4 %, c4 -2 %, c5 -0.3 %; r02_ab_xtile_prefetch.json)
                         if (kc + STAGES - 1 + PFD < nk)
                             prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + PFD, nk, rt & 1));
                     }
