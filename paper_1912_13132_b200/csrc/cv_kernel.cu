@@ -51,6 +51,7 @@
 // pivots) shares the FP64 pipe with DMMA, so it is kept short: a table-driven exp for
 // x <= 0 and branch-free generation.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 
@@ -65,6 +66,9 @@ constexpr int KC = 16;       // = the column-group width of the factor layout
 #define PGPCV_PFD 4
 #endif
 constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (chunks)
+#ifndef PGPCV_PFD_SMALL  // the same for the small-subset kernel (Geo<64, 32, ...>)
+#define PGPCV_PFD_SMALL PGPCV_PFD
+#endif
 
 // Kernel geometry.  Two instantiations:
 //   Geo<128, 64, 2>: the large-subset kernel -- 8 warps, row tiles of MT = 128, block
@@ -78,6 +82,7 @@ template <int MT_, int NB_, int MINB_, bool BORDER_, int STAGES_ = 3, bool SIG_ 
 struct Geo {
     static constexpr int MT = MT_, NB = NB_, MINB = MINB_;
     static constexpr bool BORDER = BORDER_;  // bordered prediction compiled in
+    static constexpr int PFD = MT_ == 64 ? PGPCV_PFD_SMALL : PGPCV_PFD;  // L2 prefetch distance
     static constexpr bool SIG = SIG_;        // covariance entries read from the per-range blocks
     // Warp-specialised CTA (WS): two consumer groups of NWARP warps, each an independent
     // "virtual CTA" with its own item, SMEM and named barrier, plus a producer warpgroup whose
@@ -297,7 +302,7 @@ __device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage
     constexpr int PRO = PGPCV_LAST_REFILLS == 1 ? G::STAGES : G::STAGES - 1;  // chunks in flight at tile start
     for (int i = 0; i < min(PRO, nk); ++i)
         issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev));
-    for (int i = PRO; i < min(PRO + PFD, nk); ++i)
+    for (int i = PRO; i < min(PRO + G::PFD, nk); ++i)
         prefetch_chunk<G>(L, ld, r0, j0, chunk_col(i, nk, rev));
 }
 
@@ -608,8 +613,8 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                                            chunk_col(kc + STAGES - 1, nk, rt & 1));
                         // (running this L2 prefetch on into the next row tile's first chunks
                         // measured slower: c3 -4 %, c4 -2 %, c5 -0.3 %; r02_ab_xtile_prefetch.json)
-                        if (kc + STAGES - 1 + PFD < nk)
-                            prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + PFD, nk, rt & 1));
+                        if (kc + STAGES - 1 + G::PFD < nk)
+                            prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + G::PFD, nk, rt & 1));
                     }
                     PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
@@ -657,8 +662,8 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                             if (kc + STAGES < nk)
                                 issue_chunk<G>(n + STAGES, stage, full, empty, L, ld, r0, j0,
                                                chunk_col(kc + STAGES, nk, rt & 1));
-                            if (kc + STAGES + PFD < nk)
-                                prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES + PFD, nk, rt & 1));
+                            if (kc + STAGES + G::PFD < nk)
+                                prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES + G::PFD, nk, rt & 1));
                         }
 #endif
                     }
@@ -1267,24 +1272,40 @@ __global__ void __launch_bounds__(256) sigma_kernel(const int32_t *subs, int32_t
 
 // out[c] = sum_s vals[s, c] in ascending s (Alg.1 line 9) over the subsets the
 // mask admits (mask_off[s+1] > mask_off[s], i.e. subsets with targets; all when null);
-// status[c] = the smallest failing admitted subset or -1.  One thread per config: a fixed,
-// deterministic order.
-__global__ void reduce_kernel(const double *vals, const uint8_t *fail, const int64_t *mask_off, int64_t N,
-                              int32_t C, double *out, int32_t *status) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
+// status[c] = the smallest failing admitted subset or -1.  One CTA per config: the threads
+// stage a chunk of the strided column vals[:, c] in SMEM (independent loads in flight
+// together; a single thread walking the column paid one L2 round trip per subset, ~0.9 ms at
+// c5's 2,500 subsets), then thread 0 adds the chunk in ascending s -- the same fixed,
+// deterministic order as before, bit for bit.  Entries that are not admitted or failed are
+// staged as +0.0, which leaves the running sum unchanged (it starts at +0.0, so it is never
+// -0.0); a failed admitted entry makes the result NaN anyway.
+constexpr int kReduceChunk = 2048;
+__global__ void __launch_bounds__(256) reduce_kernel(const double *vals, const uint8_t *fail, const int64_t *mask_off,
+                                                     int64_t N, int32_t C, double *out, int32_t *status) {
+    __shared__ double sv[kReduceChunk];
+    __shared__ int s_first;
+    const int c = blockIdx.x;
+    if (threadIdx.x == 0) s_first = INT_MAX;
     double acc = 0.0;
-    int64_t st = -1;
-    for (int64_t s = 0; s < N; ++s) {
-        if (mask_off && mask_off[s + 1] == mask_off[s]) continue;
-        if (fail[s * C + c]) {
-            if (st < 0) st = s;
-        } else {
-            acc += vals[s * C + c];
+    for (int64_t base = 0; base < N; base += kReduceChunk) {
+        const int n = (int)(N - base < kReduceChunk ? N - base : kReduceChunk);
+        __syncthreads();  // s_first initialised / the previous chunk summed
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int64_t s = base + i;
+            const bool admitted = !mask_off || mask_off[s + 1] != mask_off[s];
+            const bool f = admitted && fail[s * C + c];
+            if (f) atomicMin(&s_first, (int)s);
+            sv[i] = admitted && !f ? vals[s * C + c] : 0.0;
         }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < n; ++i) acc += sv[i];
     }
-    out[c] = st >= 0 ? __longlong_as_double(0x7ff8000000000000ll) : acc;
-    if (status) status[c] = (int32_t)st;
+    if (threadIdx.x == 0) {
+        const int64_t st = s_first == INT_MAX ? -1 : s_first;
+        out[c] = st >= 0 ? __longlong_as_double(0x7ff8000000000000ll) : acc;
+        if (status) status[c] = (int32_t)st;
+    }
 }
 
 // zeta dedup (pgpcv_evaluate): every configuration c takes the results of its unique
@@ -1497,7 +1518,8 @@ cudaError_t launch_device_math(int32_t fn, int64_t n, const double *x, double *y
 
 cudaError_t launch_reduce(const double *vals, const uint8_t *fail, const int64_t *mask_off, int64_t N,
                           int32_t C, double *out, int32_t *status, cudaStream_t st) {
-    reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(vals, fail, mask_off, N, C, out, status);
+    if (C <= 0) return cudaSuccess;
+    reduce_kernel<<<C, 256, 0, st>>>(vals, fail, mask_off, N, C, out, status);
     return cudaGetLastError();
 }
 
