@@ -292,6 +292,12 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 #ifndef PGPCV_SNAKE
 #define PGPCV_SNAKE 1
 #endif
+// Diagonal panel (warp 0): 1 = the pivot chain through a reciprocal estimate with the
+// correction folded into the multiplier, and Linv rows pre-scaled (shorter FP64 chains);
+// 0 = the round-1 chain through rsqrt_nb.
+#ifndef PGPCV_PIVOT_RCP
+#define PGPCV_PIVOT_RCP 0
+#endif
 __device__ __forceinline__ int chunk_col(int i, int nk, bool rev) { return (PGPCV_SNAKE && rev ? nk - 1 - i : i) * KC; }
 // Tile prologue: SMEM chunks 0..STAGES-2 and L2 prefetches of the next PFD chunks.
 template <class G>
@@ -734,6 +740,25 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                                         bad = true;
                                     } else {
                                         const double inv = rsqrt_nb(piv);
+#if PGPCV_PIVOT_RCP
+                                        // l / pivot from the hardware reciprocal estimate y0 and a
+                                        // second-order correction folded into the multiplier:
+                                        // l y0 (1 + e + e^2), e = 1 - pivot y0 -- four dependent FP64
+                                        // operations from the pivot to the next one instead of
+                                        // seven (rsqrt_nb, its square, the product); inv leaves
+                                        // the chain (it only scales the stored column)
+                                        double y0;
+                                        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(piv));
+                                        const double e1 = fma(-piv, y0, 1.0);
+                                        const double e2 = fma(e1, e1, e1);
+#pragma unroll
+                                        for (int c3 = c2 + 1; c3 < 8; ++c3) {
+                                            const double f0 = lu[c3] * y0;
+                                            const double f = fma(e2, f0, f0);
+                                            va[c3] -= va[c2] * f;
+                                            vb[c3] -= vb[c2] * f;
+                                        }
+#else
                                         const double rp = inv * inv;  // 1 / pivot
                                         // trailing columns of the panel with the unscaled column:
                                         // (u inv)(l inv) = u l / pivot
@@ -743,6 +768,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                                             va[c3] -= va[c2] * f;
                                             vb[c3] -= vb[c2] * f;
                                         }
+#endif
                                         const double sd = piv * inv;
                                         rinv[c2] = inv;
                                         if (lane == 0) dg[p0 + c2] = sd;
@@ -769,6 +795,23 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                                     w0[i] = i < pw ? RI[(p0 + i) * LJS + lane] : 0.0;
                                     w1[i] = (NB > 32 && i < pw) ? RI[(p0 + i) * LJS + lane + 32] : 0.0;
                                 }
+#if PGPCV_PIVOT_RCP
+                                // (row i pre-scaled by 1 / L_ii off the chain: one dependent
+                                // operation per row instead of two)
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    w0[i] *= rinv[i];
+                                    w1[i] *= rinv[i];
+#pragma unroll
+                                    for (int i2 = 0; i2 < i; ++i2) {
+                                        const double l = __shfl_sync(0xffffffffu, va[i2], i) * rinv[i];
+                                        w0[i] -= l * w0[i2];
+                                        w1[i] -= l * w1[i2];
+                                    }
+                                    w0[i] = lane <= p0 + i ? w0[i] : 0.0;
+                                    w1[i] = lane + 32 <= p0 + i ? w1[i] : 0.0;
+                                }
+#else
 #pragma unroll
                                 for (int i = 0; i < 8; ++i) {
 #pragma unroll
@@ -780,6 +823,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                                     w0[i] = lane <= p0 + i ? w0[i] * rinv[i] : 0.0;
                                     w1[i] = lane + 32 <= p0 + i ? w1[i] * rinv[i] : 0.0;
                                 }
+#endif
 #pragma unroll
                                 for (int i = 0; i < 8; ++i) {
                                     if (i < pw && lane <= p0 + i) RI[(p0 + i) * LJS + lane] = w0[i];

@@ -12,6 +12,10 @@ Plans:
            c5 #4 = (0.5, 0.5, 0.2): lambda 0.4) on 40 stratified subsets, and c4 #60
            (range 1, lambda 0.0125) on 48 stratified subsets.  ~40 min of oracle time on 16
            cores.
+  grids    the WHOLE parameter grid on EVERY subset at c3 (1,600 subsets) and c4 (10,000
+           subsets, k up to ~2,000): one representative of each bit-distinct (range, lambda)
+           of the grid -- every factorization a whole-grid call executes (R26) -- with the
+           global losses.  ~30 min of oracle time on 16 cores.
 Any entry beyond 1e-9 is adjudicated with the long-double (x87 80-bit) oracle and reported
 with ||e||, m and a kappa estimate (SURVEY 8(c) #18); the bar is never loosened."""
 import argparse
@@ -159,14 +163,41 @@ def plan_c5_full(ctx, out):
     print("c4 #60", json.dumps(e), file=sys.stderr, flush=True)
 
 
+def plan_grids(ctx, out):
+    for name in ("c3", "c4"):
+        t0 = time.time()
+        w = workloads.make(name, device="cuda")
+        ref_part, member_ok = _part(ctx, w)
+        # one representative per bit-distinct (range, lambda = nugget / sigma2) (R26)
+        zeta = np.stack([w.params[:, 0], w.params[:, 2] / w.params[:, 1]], axis=1)
+        _, rep = np.unique(zeta, axis=0, return_index=True)
+        rep = np.sort(rep)
+        params = np.ascontiguousarray(w.params[rep])
+        res = ctx.cv_loss(params)
+        ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, params, threads=THREADS)
+        lam = params[:, 2] / params[:, 1]
+        entry = {"membership_bit_exact": member_ok, "subsets": int(ref_part.n_subsets),
+                 "grid_configs": int(len(w.params)), "distinct_range_lambda": int(len(rep)),
+                 "config_indices": rep.tolist(),
+                 "range_minmax": [float(params[:, 0].min()), float(params[:, 0].max())],
+                 "lambda_minmax": [float(lam.min()), float(lam.max())],
+                 **compare(w, ref_part, res, ref, np.arange(ref_part.n_subsets), params),
+                 "max_rel_err_global": float(np.max(np.abs(res.loss - ref.loss) / np.abs(ref.loss))),
+                 "status_all_ok": bool(np.all(res.status == -1)),
+                 "k_range": [int(ref_part.k().min()), int(ref_part.k().max())],
+                 "seconds": round(time.time() - t0, 1)}
+        out["configs"][name + "_whole_grid_all_subsets"] = entry
+        print(name, json.dumps(entry), file=sys.stderr, flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--plan", default="sampled", choices=["sampled", "c5_full"])
+    ap.add_argument("--plan", default="sampled", choices=["sampled", "c5_full", "grids"])
     args = ap.parse_args()
     out = {"tolerance": "per-subset and global loss |g - o| <= 1e-9 |o|; membership bit-exact",
            "plan": args.plan, "oracle_threads": THREADS, "configs": {}}
     with pg.Context(0) as ctx:
-        (plan_c5_full if args.plan == "c5_full" else plan_sampled)(ctx, out)
+        {"c5_full": plan_c5_full, "grids": plan_grids, "sampled": plan_sampled}[args.plan](ctx, out)
     print(json.dumps(out, indent=1))
 
 
