@@ -292,6 +292,9 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 #ifndef PGPCV_SNAKE
 #define PGPCV_SNAKE 1
 #endif
+#ifndef PGPCV_RUNAHEAD  // the operand ring runs on across row tiles (see the update loop)
+#define PGPCV_RUNAHEAD 1
+#endif
 // Diagonal panel (warp 0): 1 = the pivot chain through a reciprocal estimate with the
 // correction folded into the multiplier, and Linv rows pre-scaled (shorter FP64 chains);
 // 0 = the round-1 chain through rsqrt_nb.
@@ -300,13 +303,14 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 #endif
 __device__ __forceinline__ int chunk_col(int i, int nk, bool rev) { return (PGPCV_SNAKE && rev ? nk - 1 - i : i) * KC; }
 // Tile prologue: SMEM chunks 0..STAGES-2 and L2 prefetches of the next PFD chunks.
+// (issued = true: the previous tile's update loop already issued the SMEM chunks, PGPCV_RUNAHEAD)
 template <class G>
 __device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage, uint64_t *full,
                                               uint64_t *empty, const double *L, int64_t ld, int r0,
-                                              int j0, bool rev) {
+                                              int j0, bool rev, bool issued = false) {
     fence_proxy_async();
     constexpr int PRO = PGPCV_LAST_REFILLS == 1 ? G::STAGES : G::STAGES - 1;  // chunks in flight at tile start
-    for (int i = 0; i < min(PRO, nk); ++i)
+    for (int i = 0; i < min(PRO, nk) && !issued; ++i)
         issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev));
     for (int i = PRO; i < min(PRO + G::PFD, nk); ++i)
         prefetch_chunk<G>(L, ld, r0, j0, chunk_col(i, nk, rev));
@@ -611,12 +615,22 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                 PH(2);
                 // acc += L[r0:r0+MT, 0:j0] . L[j0:j0+NB, 0:j0]^T
                 const int sw = (g & 3) << 2;  // fragment swizzle (row & 3 == g & 3)
+                // Run-ahead: from row tile 1 on, the operand ring runs on into the next row
+                // tile of the block column (its operands are earlier block columns, final
+                // since the column's start), so the first chunks of tile rt + 1 are in flight
+                // during the last chunks of tile rt instead of from its TRSM on.  Not from
+                // tile 0: the diagonal block reuses the stage memory between the two.
+                const bool run_next = PGPCV_RUNAHEAD && PGPCV_LAST_REFILLS == 0 && !G::WS && rt >= 1 &&
+                                      rt + 1 < ntiles && nk >= STAGES - 1;
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
                     if (!G::WS && tid == 0 && (PGPCV_LAST_REFILLS != 1) && (PGPCV_LAST_REFILLS == 0 || kc == 0)) {
                         if (kc + STAGES - 1 < nk)
                             issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
                                            chunk_col(kc + STAGES - 1, nk, rt & 1));
+                        else if (run_next)
+                            issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0 + MT, j0,
+                                           chunk_col(kc + STAGES - 1 - nk, nk, (rt + 1) & 1));
                         // (running this L2 prefetch on into the next row tile's first chunks
                         // measured slower: c3 -4 %, c4 -2 %, c5 -0.3 %; r02_ab_xtile_prefetch.json)
                         if (kc + STAGES - 1 + G::PFD < nk)
@@ -919,7 +933,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
                 if (!G::WS && rt + 1 < ntiles && tid == 0)
-                    tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1);
+                    tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1, run_next);
                 if constexpr (G::SIG) {  // the next tile's covariance entries into L2
                     if (tid == 0) {
                         if (rt + 1 < ntiles) sig_prefetch(r0 + MT, j0);
