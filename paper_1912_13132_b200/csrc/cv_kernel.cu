@@ -292,8 +292,15 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 #ifndef PGPCV_SNAKE
 #define PGPCV_SNAKE 1
 #endif
-#ifndef PGPCV_RUNAHEAD  // the operand ring runs on across row tiles (see the update loop)
-#define PGPCV_RUNAHEAD 1
+#ifndef PGPCV_ISSUE_AT
+#define PGPCV_ISSUE_AT 0
+#endif
+// 1 = the operand ring runs on across row tiles (see the update loop).  Measured slower on
+// the same box (c3 -3.9 %, c4 -0.7 %, c5 -0.4 %; profiles/r02d_ab_runahead.json): thread 0
+// then waits for every warp's release in the last chunks of a tile too, where it otherwise
+// catches up with the other warps.  Off.
+#ifndef PGPCV_RUNAHEAD
+#define PGPCV_RUNAHEAD 0
 #endif
 // Diagonal panel (warp 0): 1 = the pivot chain through a reciprocal estimate with the
 // correction folded into the multiplier, and Linv rows pre-scaled (shorter FP64 chains);
@@ -624,7 +631,11 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                                       rt + 1 < ntiles && nk >= STAGES - 1;
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint32_t n = pc + kc;
-                    if (!G::WS && tid == 0 && (PGPCV_LAST_REFILLS != 1) && (PGPCV_LAST_REFILLS == 0 || kc == 0)) {
+                    // (PGPCV_ISSUE_AT: thread 0 refills at the start of the chunk (0) or after
+                    // that many of its warp's k-slices, when the other warps have more likely
+                    // released the stage already)
+                    auto refill = [&]() {
+                      if (!G::WS && tid == 0 && (PGPCV_LAST_REFILLS != 1) && (PGPCV_LAST_REFILLS == 0 || kc == 0)) {
                         if (kc + STAGES - 1 < nk)
                             issue_chunk<G>(n + STAGES - 1, stage, full, empty, L, ld, r0, j0,
                                            chunk_col(kc + STAGES - 1, nk, rt & 1));
@@ -635,7 +646,9 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                         // measured slower: c3 -4 %, c4 -2 %, c5 -0.3 %; r02_ab_xtile_prefetch.json)
                         if (kc + STAGES - 1 + G::PFD < nk)
                             prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + G::PFD, nk, rt & 1));
-                    }
+                      }
+                    };
+                    if (PGPCV_ISSUE_AT == 0) refill();
                     PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
                     PH(4);
@@ -648,6 +661,10 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                     if (live) {
 #pragma unroll
                         for (int k4 = 0; k4 < KC / 4; ++k4) {
+                            if (PGPCV_ISSUE_AT > 0 && k4 == PGPCV_ISSUE_AT) {  // (warp 0 is always live)
+                                refill();
+                                __syncwarp();
+                            }
                             const int o = (k4 << 2) ^ sw;
                             double af[2], bf[NJ];
                             af[0] = ap[o];

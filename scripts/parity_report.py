@@ -16,6 +16,8 @@ Plans:
            subsets, k up to ~2,000): one representative of each bit-distinct (range, lambda)
            of the grid -- every factorization a whole-grid call executes (R26) -- with the
            global losses.  ~30 min of oracle time on 16 cores.
+  c5_corner c5 at the grid's worst-conditioned corner (#120 = (2, 2, 0.05): range 2, lambda
+           0.025, kappa ~ 1e5) over ALL 2,500 subsets with the global loss.  ~35 min of oracle.
 Any entry beyond 1e-9 is adjudicated with the long-double (x87 80-bit) oracle and reported
 with ||e||, m and a kappa estimate (SURVEY 8(c) #18); the bar is never loosened."""
 import argparse
@@ -163,6 +165,26 @@ def plan_c5_full(ctx, out):
     print("c4 #60", json.dumps(e), file=sys.stderr, flush=True)
 
 
+def plan_c5_corner(ctx, out):
+    w = workloads.make("c5", device="cuda")
+    ref_part, member_ok = _part(ctx, w)
+    k, m = ref_part.k(), ref_part.m()
+    t0 = time.time()
+    p = w.params[[120]]
+    res = ctx.cv_loss(p)
+    ref = oracle.cv_loss(w.x, w.y, w.value, ref_part, p, threads=THREADS)
+    big = int(np.argmax(k))
+    e = {"membership_bit_exact": member_ok, "config_index": 120, "config": p[0].tolist(),
+         **compare(w, ref_part, res, ref, np.arange(ref_part.n_subsets), p),
+         "loss_gpu": float(res.loss[0]), "loss_oracle": float(ref.loss[0]),
+         "rel_err_global": float(abs(res.loss[0] - ref.loss[0]) / abs(ref.loss[0])),
+         "kappa_max_k_subset": _kappa(w, ref_part, big, p[0]),
+         "k_range": [int(k.min()), int(k.max())], "m_range": [int(m.min()), int(m.max())],
+         "seconds": round(time.time() - t0, 1)}
+    out["configs"]["c5_cfg120_all_subsets"] = e
+    print("c5 #120 all", json.dumps(e), file=sys.stderr, flush=True)
+
+
 def plan_grids(ctx, out):
     for name in ("c3", "c4"):
         t0 = time.time()
@@ -192,12 +214,12 @@ def plan_grids(ctx, out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--plan", default="sampled", choices=["sampled", "c5_full", "grids"])
+    ap.add_argument("--plan", default="sampled", choices=["sampled", "c5_full", "grids", "c5_corner"])
     args = ap.parse_args()
     out = {"tolerance": "per-subset and global loss |g - o| <= 1e-9 |o|; membership bit-exact",
            "plan": args.plan, "oracle_threads": THREADS, "configs": {}}
     with pg.Context(0) as ctx:
-        {"c5_full": plan_c5_full, "grids": plan_grids, "sampled": plan_sampled}[args.plan](ctx, out)
+        {"c5_full": plan_c5_full, "grids": plan_grids, "c5_corner": plan_c5_corner, "sampled": plan_sampled}[args.plan](ctx, out)
     print(json.dumps(out, indent=1))
 
 
