@@ -66,6 +66,27 @@ constexpr int KC = 16;       // = the column-group width of the factor layout
 #define PGPCV_PFD 4
 #endif
 constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (chunks)
+// Where thread 0 refills the operand ring within a chunk: at its start (0) or after that many
+// of its warp's four k-slices.  The refill waits until every warp released the stage's previous
+// use, so the issuing warp starts each chunk last; a quarter chunk later the others have
+// usually released it already.  Same-box A/B (profiles/r02d_ab_issue_at.json): large kernel
+// (c5) +1.0 % at 1, +0.7 % at 2; small kernel (c3, c4) -0.6 % / -1.3 %: its short tiles need
+// the earliest issue.
+#ifndef PGPCV_ISSUE_AT_LARGE
+#define PGPCV_ISSUE_AT_LARGE 1
+#endif
+#ifndef PGPCV_ISSUE_AT_SMALL
+#define PGPCV_ISSUE_AT_SMALL 0
+#endif
+// 1 = non-blocking refills: thread 0 polls the stage's empty barrier at every k-slice and
+// issues as soon as it is free (up to STAGES - 1 chunks ahead); it blocks only for the chunk
+// it is about to consume.
+#ifndef PGPCV_POLL_LARGE
+#define PGPCV_POLL_LARGE 0
+#endif
+#ifndef PGPCV_POLL_SMALL
+#define PGPCV_POLL_SMALL 0
+#endif
 #ifndef PGPCV_PFD_SMALL  // the same for the small-subset kernel (Geo<64, 32, ...>)
 #define PGPCV_PFD_SMALL PGPCV_PFD
 #endif
@@ -83,6 +104,8 @@ struct Geo {
     static constexpr int MT = MT_, NB = NB_, MINB = MINB_;
     static constexpr bool BORDER = BORDER_;  // bordered prediction compiled in
     static constexpr int PFD = MT_ == 64 ? PGPCV_PFD_SMALL : PGPCV_PFD;  // L2 prefetch distance
+    static constexpr int ISSUE_AT = MT_ == 64 ? PGPCV_ISSUE_AT_SMALL : PGPCV_ISSUE_AT_LARGE;  // refill position
+    static constexpr bool POLL = !WS_ && (MT_ == 64 ? PGPCV_POLL_SMALL : PGPCV_POLL_LARGE);  // non-blocking refills
     static constexpr bool SIG = SIG_;        // covariance entries read from the per-range blocks
     // Warp-specialised CTA (WS): two consumer groups of NWARP warps, each an independent
     // "virtual CTA" with its own item, SMEM and named barrier, plus a producer warpgroup whose
@@ -152,6 +175,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
     } while (!done);
+}
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, unsigned parity) {  // non-blocking
+    unsigned done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
 }
 // 1-D bulk copy global -> shared (async proxy), completion counted on `bar` in bytes.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
@@ -245,16 +277,22 @@ __device__ __forceinline__ const double *lchunk(const double *L, int64_t ld, int
 // rows r0..r0+MT-1 (A) and j0..j0+NB-1 (B) of column group kk/16.  Rows past the matrix
 // are copied as whatever the workspace holds; they only reach discarded outputs (see the
 // masking of acc after the update).  Chunk n + PFD is prefetched into L2.
+// (block = false: only if the stage is free already; returns whether the chunk was issued)
 template <class G>
-__device__ __forceinline__ void issue_chunk(uint32_t n, double *stage, uint64_t *full, uint64_t *empty,
-                                            const double *L, int64_t ld, int r0, int j0, int kk) {
+__device__ __forceinline__ bool issue_chunk(uint32_t n, double *stage, uint64_t *full, uint64_t *empty,
+                                            const double *L, int64_t ld, int r0, int j0, int kk,
+                                            bool block = true) {
     const int sidx = n % G::STAGES;
     const uint32_t use = n / G::STAGES;
-    if (use > 0) mbar_wait(&empty[sidx], (use - 1) & 1);
+    if (use > 0) {
+        if (block) mbar_wait(&empty[sidx], (use - 1) & 1);
+        else if (!mbar_test(&empty[sidx], (use - 1) & 1)) return false;
+    }
     double *sb = stage + sidx * (G::A_STAGE + G::B_STAGE);
     mbar_expect_tx(&full[sidx], G::STAGE_BYTES);
     bulk_g2s(sb, lchunk(L, ld, kk / KC, r0), G::MT * KC * sizeof(double), &full[sidx]);
     bulk_g2s(sb + G::A_STAGE, lchunk(L, ld, kk / KC, j0), G::NB * KC * sizeof(double), &full[sidx]);
+    return true;
 }
 template <class G>
 __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int r0, int j0, int kk) {
@@ -292,9 +330,6 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 #ifndef PGPCV_SNAKE
 #define PGPCV_SNAKE 1
 #endif
-#ifndef PGPCV_ISSUE_AT
-#define PGPCV_ISSUE_AT 0
-#endif
 // 1 = the operand ring runs on across row tiles (see the update loop).  Measured slower on
 // the same box (c3 -3.9 %, c4 -0.7 %, c5 -0.4 %; profiles/r02d_ab_runahead.json): thread 0
 // then waits for every warp's release in the last chunks of a tile too, where it otherwise
@@ -311,16 +346,21 @@ __device__ __forceinline__ void prefetch_chunk(const double *L, int64_t ld, int 
 __device__ __forceinline__ int chunk_col(int i, int nk, bool rev) { return (PGPCV_SNAKE && rev ? nk - 1 - i : i) * KC; }
 // Tile prologue: SMEM chunks 0..STAGES-2 and L2 prefetches of the next PFD chunks.
 // (issued = true: the previous tile's update loop already issued the SMEM chunks, PGPCV_RUNAHEAD)
+// Returns the number of SMEM chunks issued (POLL: only those whose stage was free).
 template <class G>
-__device__ __forceinline__ void tile_prologue(uint32_t pc, int nk, double *stage, uint64_t *full,
-                                              uint64_t *empty, const double *L, int64_t ld, int r0,
-                                              int j0, bool rev, bool issued = false) {
+__device__ __forceinline__ int tile_prologue(uint32_t pc, int nk, double *stage, uint64_t *full,
+                                             uint64_t *empty, const double *L, int64_t ld, int r0,
+                                             int j0, bool rev, bool issued = false) {
     fence_proxy_async();
     constexpr int PRO = PGPCV_LAST_REFILLS == 1 ? G::STAGES : G::STAGES - 1;  // chunks in flight at tile start
-    for (int i = 0; i < min(PRO, nk) && !issued; ++i)
-        issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev));
+    int ni = 0;
+    for (int i = 0; i < min(PRO, nk) && !issued; ++i) {
+        if (!issue_chunk<G>(pc + i, stage, full, empty, L, ld, r0, j0, chunk_col(i, nk, rev), !G::POLL)) break;
+        ++ni;
+    }
     for (int i = PRO; i < min(PRO + G::PFD, nk); ++i)
         prefetch_chunk<G>(L, ld, r0, j0, chunk_col(i, nk, rev));
+    return ni;
 }
 
 template <class G>
@@ -406,6 +446,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsConsumerRegs) : "memory");
     }
     uint32_t pc = 0;  // operand chunks consumed so far (identical in every thread)
+    uint32_t issued = 0;  // POLL, thread 0: operand chunks issued so far
     unsigned n_claims = 0;  // WS: items this group claimed (thread 0)
     PH_DECL
 
@@ -511,7 +552,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
             // stage memory was last touched by generic accesses (LJ, alpha).
             PH(0);
             if (!G::WS && tid == 0) {  // (WS: the producer issues every chunk)
-                tile_prologue<G>(pc, nk, stage, full, empty, L, ld, j0, j0, false);
+                issued = pc + tile_prologue<G>(pc, nk, stage, full, empty, L, ld, j0, j0, false);
                 if (jb == 0) sig_prefetch(j0, j0);
             }
             __syncwarp();
@@ -648,7 +689,20 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                             prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + G::PFD, nk, rt & 1));
                       }
                     };
-                    if (PGPCV_ISSUE_AT == 0) refill();
+                    if constexpr (G::POLL) {
+                        if (tid == 0) {
+                            // the chunk about to be consumed (and any before it) must be in flight
+                            while ((int)(issued - n) <= 0) {
+                                issue_chunk<G>(issued, stage, full, empty, L, ld, r0, j0,
+                                               chunk_col((int)(issued - pc), nk, rt & 1));
+                                ++issued;
+                            }
+                            if (kc + STAGES - 1 + G::PFD < nk)
+                                prefetch_chunk<G>(L, ld, r0, j0, chunk_col(kc + STAGES - 1 + G::PFD, nk, rt & 1));
+                        }
+                    } else if (G::ISSUE_AT == 0) {
+                        refill();
+                    }
                     PH(3);
                     mbar_wait(&full[n % STAGES], (n / STAGES) & 1);
                     PH(4);
@@ -661,7 +715,13 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                     if (live) {
 #pragma unroll
                         for (int k4 = 0; k4 < KC / 4; ++k4) {
-                            if (PGPCV_ISSUE_AT > 0 && k4 == PGPCV_ISSUE_AT) {  // (warp 0 is always live)
+                            if constexpr (G::POLL) {  // (warp 0 is always live)
+                                if (tid == 0 && (int)(issued - pc) <= min(kc + STAGES - 1, nk - 1) &&
+                                    issue_chunk<G>(issued, stage, full, empty, L, ld, r0, j0,
+                                                   chunk_col((int)(issued - pc), nk, rt & 1), false))
+                                    ++issued;
+                                __syncwarp();
+                            } else if (G::ISSUE_AT > 0 && k4 == G::ISSUE_AT) {
                                 refill();
                                 __syncwarp();
                             }
@@ -950,7 +1010,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
                 if (!G::WS && rt + 1 < ntiles && tid == 0)
-                    tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1, run_next);
+                    issued = pc + tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1, run_next);
                 if constexpr (G::SIG) {  // the next tile's covariance entries into L2
                     if (tid == 0) {
                         if (rt + 1 < ntiles) sig_prefetch(r0 + MT, j0);
