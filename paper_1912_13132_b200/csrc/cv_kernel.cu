@@ -69,8 +69,8 @@ constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (
 // Where thread 0 refills the operand ring within a chunk: at its start (0) or after that many
 // of its warp's four k-slices.  The refill waits until every warp released the stage's previous
 // use, so the issuing warp starts each chunk last; a quarter chunk later the others have
-// usually released it already.  Same-box A/B (profiles/r02d_ab_issue_at.json): large kernel
-// (c5) +1.0 % at 1, +0.7 % at 2; small kernel (c3, c4) -0.6 % / -1.3 %: its short tiles need
+// usually released it already.  Same-box A/B (profiles/r02d_ab_issue_at.json, reproduced in
+// r02d_ab_poll.json): large kernel (c5) +1.0 % at 1, +0.7 % at 2; small kernel (c3, c4) -0.6 % / -1.3 %: its short tiles need
 // the earliest issue.
 #ifndef PGPCV_ISSUE_AT_LARGE
 #define PGPCV_ISSUE_AT_LARGE 1
@@ -80,7 +80,10 @@ constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (
 #endif
 // 1 = non-blocking refills: thread 0 polls the stage's empty barrier at every k-slice and
 // issues as soon as it is free (up to STAGES - 1 chunks ahead); it blocks only for the chunk
-// it is about to consume.
+// it is about to consume.  Measured slower on the same box (large kernel, c5: -2.3 % against
+// ISSUE_AT 0, -3.2 % against ISSUE_AT 1; small kernel, c3: -14 %, c4: -6.5 %;
+// profiles/r02d_ab_poll.json): the polls and their warp re-convergence sit in warp 0's DMMA
+// stream.  Off.
 #ifndef PGPCV_POLL_LARGE
 #define PGPCV_POLL_LARGE 0
 #endif
