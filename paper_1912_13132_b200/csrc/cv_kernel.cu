@@ -78,9 +78,6 @@ constexpr int PFD = PGPCV_PFD;  // L2 prefetch distance beyond the SMEM stages (
 #ifndef PGPCV_ISSUE_AT_SMALL
 #define PGPCV_ISSUE_AT_SMALL 0
 #endif
-#ifndef PGPCV_PROLOGUE_AT_LARGE  // see next_prologue in the kernel
-#define PGPCV_PROLOGUE_AT_LARGE 0
-#endif
 // 1 = non-blocking refills: thread 0 polls the stage's empty barrier at every k-slice and
 // issues as soon as it is free (up to STAGES - 1 chunks ahead); it blocks only for the chunk
 // it is about to consume.  Measured slower on the same box (large kernel, c5: -2.3 % against
@@ -112,7 +109,6 @@ struct Geo {
     static constexpr int PFD = MT_ == 64 ? PGPCV_PFD_SMALL : PGPCV_PFD;  // L2 prefetch distance
     static constexpr int ISSUE_AT = MT_ == 64 ? PGPCV_ISSUE_AT_SMALL : PGPCV_ISSUE_AT_LARGE;  // refill position
     static constexpr bool POLL = !WS_ && (MT_ == 64 ? PGPCV_POLL_SMALL : PGPCV_POLL_LARGE);  // non-blocking refills
-    static constexpr int PRO_AT = MT_ == 64 ? 0 : PGPCV_PROLOGUE_AT_LARGE;  // next tile's prologue position
     static constexpr bool SIG = SIG_;        // covariance entries read from the per-range blocks
     // Warp-specialised CTA (WS): two consumer groups of NWARP warps, each an independent
     // "virtual CTA" with its own item, SMEM and named barrier, plus a producer warpgroup whose
@@ -1016,13 +1012,8 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
 
                 // Prefetch the next row tile's first chunks (same block column: they read
                 // only earlier block columns) so their latency hides behind the TRSM.
-                // (PRO_AT: before the TRSM (0), between its two 32-column halves (1), after it (2):
-                // the prologue waits until every warp finished the tile's update)
-                auto next_prologue = [&]() {
-                    if (!G::WS && rt + 1 < ntiles && tid == 0)
-                        issued = pc + tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1, run_next);
-                };
-                if (G::PRO_AT == 0) next_prologue();
+                if (!G::WS && rt + 1 < ntiles && tid == 0)
+                    issued = pc + tile_prologue<G>(pc, nk, stage, full, empty, L, ld, r0 + MT, j0, (rt + 1) & 1, run_next);
                 if constexpr (G::SIG) {  // the next tile's covariance entries into L2
                     if (tid == 0) {
                         if (rt + 1 < ntiles) sig_prefetch(r0 + MT, j0);
@@ -1041,10 +1032,6 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                 const bool odd = t & 1;
 #pragma unroll
                 for (int h = 0; h < NB / 32; ++h) {
-                    if (G::PRO_AT == 1 && h == NB / 32 - 1) {
-                        next_prologue();
-                        __syncwarp();
-                    }
                     double xo[2][4][2];
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
@@ -1090,10 +1077,6 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) cv_kernel(CvArgs a) {
                                 }
                             }
                         }
-                }
-                if (G::PRO_AT == 2) {
-                    next_prologue();
-                    __syncwarp();
                 }
                 PH(8);
                 if (rt == ntiles - 1) {
