@@ -37,7 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # ncu --set full capture of the dominant kernel (dram bytes per launch -> roofline.traffic)
-PROFILE_JSON = "r02b_cv_kernel_c5_ncu.json"
+PROFILE_JSON = "r02e_cv_kernel_c5_ncu.json"
 METRIC = "subset CV-loss evals/sec at 5M pts (sec per param config and FP64 % of peak alongside)"
 METRICS = {"cv": METRIC,
            "cv_nll": "subset CV-loss + -2 log-lik evals/sec (one factorization per subset and config)",
